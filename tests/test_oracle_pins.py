@@ -1,0 +1,224 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+No GPU, no product code: only oracle/ and the shared input generator.  Each
+pin is chosen so that a plausible oracle bug fails it:
+  * hash constants / rotation / size terms  -> splitmix64 vectors, closed-form hashes
+  * a dropped maximality check or wrong P'/Q' threshold (Z3) -> brute force, crown 2^n-2
+  * empty-side emission (Z1) -> isolated-vertex and brute-force comparisons
+  * orientation / relabel mistakes -> side swap + candidate side metamorphic tests
+  * wrong root-restriction shortcut -> plain literal MBEA gives the same tree
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import reference as R
+from paper_2401_05039_b200 import inputs as I
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _read_golden(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+def spec_path():
+    """SPEC S:283 path: rows a0,a1; cols b0,b1; edges a0b0, a0b1, a1b1."""
+    return I.from_edges(2, 2, [0, 0, 1], [0, 1, 1], name="spec_path")
+
+
+def _closed_form_graph(name):
+    if name.startswith("crown"):
+        return I.crown(int(name[5:]))
+    if name.startswith("match"):
+        return I.perfect_matching(int(name[5:]))
+    if name == "spec_path":
+        return spec_path()
+    m, n = name[1:].split(",")
+    return I.complete(int(m), int(n))
+
+
+# ------------------------------------------------------------------ mix64
+def test_mix64_published_splitmix64_vectors():
+    G = 0x9E3779B97F4A7C15
+    for k, v in _read_golden("splitmix64_seed0.txt"):
+        z = (int(k) * G) & R.MASK64
+        assert R.mix64(z) == int(v, 16)
+        assert oracle.mix64(z) == int(v, 16)
+
+
+# ------------------------------------------------------------------ closed forms
+@pytest.mark.parametrize("row", _read_golden("closed_forms.txt"), ids=lambda r: r[0])
+def test_closed_form_golden(row):
+    name, count, h = row[0], int(row[1]), int(row[2], 16)
+    g = _closed_form_graph(name)
+    r = oracle.mbea(g, check=True)
+    assert (r.count, r.hash, r.bad) == (count, h, 0)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 6, 8, 10, 12])
+def test_crown_closed_form(n):
+    # M(S_n) = {(S, [n] \ S) : ∅ ≠ S ⊊ [n]}  ->  2^n - 2 bicliques
+    fam = []
+    for S in range(1, (1 << n) - 1):
+        A = tuple(i for i in range(n) if S >> i & 1)
+        B = tuple(j for j in range(n) if not S >> j & 1)
+        fam.append((A, B))
+    g = I.crown(n)
+    r = oracle.mbea(g)
+    assert r.count == (1 << n) - 2
+    assert r.hash == R.result_hash(fam)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 7), (3, 5), (6, 2), (9, 9)])
+def test_complete_closed_form(m, n):
+    g = I.complete(m, n)
+    r = oracle.mbea(g)
+    assert r.count == 1
+    assert r.hash == R.biclique_hash(tuple(range(m)), tuple(range(n)))
+
+
+@pytest.mark.parametrize("n", [1, 5, 17])
+def test_matching_closed_form(n):
+    r = oracle.mbea(I.perfect_matching(n))
+    assert r.count == n
+    assert r.hash == R.result_hash([((i,), (i,)) for i in range(n)])
+
+
+@pytest.mark.parametrize("m", [3, 4, 5, 8, 13])
+def test_path_closed_form(m):
+    # a path with m vertices has m-2 maximal bicliques (the stars of its inner vertices)
+    assert oracle.mbea(I.path(m)).count == m - 2
+
+
+def test_disjoint_blocks_and_star():
+    g = I.disjoint_blocks([(2, 3), (1, 1), (4, 2), (3, 3)])
+    assert oracle.mbea(g).count == 4
+    s = I.star(6)
+    r = oracle.mbea(s)
+    assert r.count == 1 and r.hash == R.biclique_hash((0,), tuple(range(6)))
+
+
+def test_empty_graphs():
+    for n1, n2 in [(0, 0), (0, 5), (4, 0), (5, 7)]:
+        g = I.from_edges(n1, n2, [], [])
+        r = oracle.mbea(g)
+        assert (r.count, r.hash, r.tasks) == (0, 0, 0)
+
+
+# ------------------------------------------------------------------ brute force
+def _random_graphs(n_graphs, max_side, seed0):
+    ps = [0.1, 0.3, 0.5, 0.7, 0.9]
+    for k in range(n_graphs):
+        z = R.mix64(seed0 + k)
+        n1 = 1 + z % max_side
+        n2 = 1 + (z >> 8) % max_side
+        yield I.random_bipartite(n1, n2, ps[k % 5], seed0 * 1000 + k)
+
+
+def test_oracle_equals_closure_bruteforce_1000_graphs():
+    """>= 1,000 random graphs, sides <= 10, p in 0.1-0.9, fixed seeds."""
+    for g in _random_graphs(1000, 10, 11):
+        truth = R.maximal_bicliques_closure(g)
+        lst = oracle.mbea_list(g)
+        assert len(lst) == len(set(lst)), "duplicate emission"
+        assert set(lst) == truth
+        r = oracle.mbea(g, threads=2, check=True)
+        assert r.count == len(truth)
+        assert r.hash == R.result_hash(truth)
+        assert r.bad == 0
+
+
+def test_oracle_orders_and_sides_agree_with_bruteforce():
+    for g in _random_graphs(300, 12, 23):
+        truth = R.maximal_bicliques_closure(g)
+        h = R.result_hash(truth)
+        for side in (1, 2):
+            for order in ("ascending", "input"):
+                r = oracle.mbea(g, candidate_side=side, order=order)
+                assert (r.count, r.hash) == (len(truth), h)
+
+
+def test_next_closure_equals_closure_bruteforce():
+    for g in _random_graphs(200, 9, 37):
+        assert R.maximal_bicliques_next_closure(g) == R.maximal_bicliques_closure(g)
+
+
+def test_plain_literal_mbea_same_tree_as_root_shortcut():
+    """The root 2-hop restriction is exact: same result AND same search tree."""
+    for g in list(_random_graphs(100, 14, 41)) + [I.crown(8), I.erdos_renyi_c1b(60, 60)]:
+        a = oracle.mbea(g)
+        b = oracle.mbea_plain(g)
+        assert (a.count, a.hash, a.tasks, a.pruned) == (b.count, b.hash, b.tasks, b.pruned)
+        assert b.bad == 0
+
+
+# ------------------------------------------------------------------ C1b golden
+def test_c1b_golden_next_closure_and_mbea():
+    gold = {k: v for k, v in _read_golden("c1b_er200.txt")}
+    g = I.erdos_renyi_c1b()
+    assert g.n_edges == int(gold["edges"])
+    nc = R.maximal_bicliques_next_closure(g)
+    assert len(nc) == int(gold["count"])
+    assert R.result_hash(nc) == int(gold["hash"], 16)
+    for side in (1, 2):
+        r = oracle.mbea(g, candidate_side=side, check=True)
+        assert (r.count, r.hash, r.bad) == (int(gold["count"]), int(gold["hash"], 16), 0)
+
+
+# ------------------------------------------------------------------ metamorphic
+def test_metamorphic_swap_isolated_duplicates_permutation():
+    g = I.erdos_renyi_c1b(80, 50)
+    base = oracle.mbea(g)
+    # swap sides: hash of the transposed set = hash with A/B roles swapped
+    gt = g.transpose()
+    lst = oracle.mbea_list(g)
+    swapped = [(B, A) for A, B in lst]
+    assert oracle.mbea(gt).hash == R.result_hash(swapped)
+    assert oracle.mbea(gt).count == base.count
+    # isolated vertices appended on both sides
+    e = g.edges()
+    gi = I.from_edges(g.n1 + 7, g.n2 + 3, e[:, 0], e[:, 1])
+    assert (oracle.mbea(gi).count, oracle.mbea(gi).hash) == (base.count, base.hash)
+    # duplicate edges (not deduplicated in the CSR): same result
+    gd = I.from_edges(g.n1, g.n2, np.concatenate([e[:, 0], e[:40, 0]]), np.concatenate([e[:, 1], e[:40, 1]]),
+                      dedup=False)
+    assert gd.n_edges == g.n_edges + 40
+    assert (oracle.mbea(gd).count, oracle.mbea(gd).hash) == (base.count, base.hash)
+    # permuted ids: map the listing back
+    rng = np.random.default_rng(5)
+    p1 = rng.permutation(g.n1)
+    p2 = rng.permutation(g.n2)
+    gp = I.from_edges(g.n1, g.n2, p1[e[:, 0]], p2[e[:, 1]])
+    mapped = {(tuple(sorted(int(p1[a]) for a in A)), tuple(sorted(int(p2[b]) for b in B))) for A, B in lst}
+    assert set(oracle.mbea_list(gp)) == mapped
+
+
+def test_per_root_sums_equal_total():
+    g = I.erdos_renyi_c1b()
+    for side in (1, 2):
+        tot = oracle.mbea(g, candidate_side=side)
+        n = g.n1 if side == 1 else g.n2
+        pr = oracle.mbea_roots(g, np.arange(n), candidate_side=side)
+        assert int(pr[:, 0].sum()) == tot.count
+        assert int(pr[:, 1].astype(object).sum()) & R.MASK64 == tot.hash
+        assert int(pr[:, 2].sum()) == tot.tasks
+        assert int(pr[:, 3].sum()) == tot.pruned
+
+
+def test_invalid_input_rejected():
+    g = I.from_edges(2, 2, [0, 1], [0, 1])
+    bad = I.Graph(2, 2, g.row_ptr, np.array([0, 5], dtype=np.uint32))
+    with pytest.raises(ValueError):
+        oracle.mbea(bad)
+    bad2 = I.Graph(2, 2, np.array([0, 2, 1], dtype=np.uint64), np.array([0, 1], dtype=np.uint32))
+    with pytest.raises(ValueError):
+        oracle.mbea(bad2)
