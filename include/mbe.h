@@ -1,0 +1,136 @@
+/* include/mbe.h — C ABI of libmbe: maximal biclique enumeration on B200 (sm_100a).
+ *
+ * Problem (§II-A): input a bipartite graph G = (U ∪ V, E);
+ * output all maximal bicliques, i.e. all pairs (A, B), A ⊆ side 1, B ⊆ side 2,
+ * both nonempty, with A × B ⊆ E, A = N(B) and B = N(A) ("a biclique is maximal
+ * if it is not a proper subset of any other biclique").
+ * Method: the MBEA search of Algorithm 1 with iMBE candidate order
+ * (P:234-245), reverse scanning and coarse-grained level-1
+ * subtrees with work stealing (§III-C/D), re-designed for sm_100a
+ * (see DESIGN.md).  The library reports {count, order-independent 64-bit hash
+ * of the canonical (A,B) set}, optionally a bounded listing.
+ *
+ * Conventions
+ *  - Every function returns an int status: MBE_OK (0) or a negative code.  No
+ *    exceptions cross the ABI.  On error, *out / *res contents are unspecified
+ *    and no handle leaks; mbe_last_error_detail() gives a message.
+ *  - Handles are thread-compatible, not re-entrant: do not call two functions
+ *    on the same handle concurrently.
+ *  - No CPU fallback: when no CUDA device is usable, mbe_load_csr returns
+ *    MBE_ECUDA.
+ */
+#ifndef MBE_H_
+#define MBE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MBE_OK = 0,
+  MBE_EINVAL = -1,    /* bad argument / config (e.g. threads_per_cta not a multiple of 32, world = 0) */
+  MBE_ENOMEM = -2,    /* host or device allocation failed */
+  MBE_ECUDA = -3,     /* CUDA runtime error or no usable device */
+  MBE_EOVERFLOW = -4, /* per-warp frame arena or depth exhausted: result invalid, retry with larger arena_bytes */
+  MBE_ERANGE = -5,    /* an edge id >= n2 */
+  MBE_EDIST = -6,     /* multi-GPU claim counter unusable */
+  MBE_EINTERNAL = -7  /* device-side consistency check failed (a bug; never a silent wrong count) */
+};
+
+/* Opaque handle: the graph resident on one device plus the search workspace. */
+typedef struct mbe_graph mbe_graph;
+
+/* Load a bipartite graph given as a row-CSR over ORIGINAL 0-based ids:
+ *   side 1 = rows (n1 vertices), side 2 = cols (n2 vertices),
+ *   row i's neighbours are col_idx[row_ptr[i] .. row_ptr[i+1]).
+ * row_ptr: HOST array of n1+1 uint64, row_ptr[0] = 0, non-decreasing (else MBE_EINVAL).
+ * col_idx: HOST array of row_ptr[n1] uint32, each < n2 (else MBE_ERANGE).
+ * Rows need not be sorted; duplicate edges are allowed and collapse to one
+ * (reading Z8); isolated vertices contribute nothing; n1 = 0, n2 = 0 or no
+ * edges is a valid empty graph (count 0, hash 0).
+ * The caller keeps ownership of both arrays (they are copied before return).
+ * device: CUDA ordinal.  flags: reserved, pass 0.
+ * Ingest builds both CSR directions (sorted, deduplicated),
+ * relabels the candidate side by ascending (degree, original id) and uploads
+ * everything to device memory owned by the handle. */
+int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t *row_ptr, const uint32_t *col_idx, int device,
+                 uint32_t flags, mbe_graph **out);
+
+/* mbe_config.flags */
+#define MBE_NO_STEAL 0x1u     /* disable inter-warp work stealing (result-invariant) */
+#define MBE_STATS 0x2u        /* count algorithmic bytes / task kinds (small overhead) */
+#define MBE_NO_ANTICHAIN 0x4u /* keep every Q' row instead of the antichain (result-invariant, slower) */
+#define MBE_NO_TWIN 0x8u      /* disable root-level twin pre-pruning (result-invariant) */
+
+typedef struct {
+  uint32_t struct_size;      /* ABI versioning: sizeof(mbe_config) */
+  uint32_t ctas_per_sm;      /* persistent CTAs per SM; 0 = auto */
+  uint32_t threads_per_cta;  /* multiple of 32, <= 1024; 0 = auto */
+  uint32_t bitmap_threshold; /* frames with |L| <= this use bit rows (<= 128); 0 = auto */
+  int32_t candidate_side;    /* 0 = auto (smaller side, ties: side 1), 1 = rows, 2 = cols; result-invariant */
+  uint32_t flags;            /* MBE_* flags above */
+  uint32_t rank, world;      /* this process' share of the level-1 subtrees (world >= 1) */
+  uint64_t *claim_counter;   /* device-visible u64 shared by all ranks (dynamic claiming; zero it before
+                                the first rank starts) or NULL (static deal: positions k = rank mod world) */
+  uint64_t arena_bytes;      /* per-warp frame arena; 0 = auto */
+  void *stream;              /* cudaStream_t to run on; NULL = the legacy default stream */
+  uint64_t *per_root;        /* optional HOST buffer [n_cand][4] = (count, hash, tasks, pruned) of each
+                                level-1 subtree, indexed by the candidate side's ORIGINAL id; or NULL */
+} mbe_config;
+
+/* Optional bounded listing; caller-owned HOST buffers.  Record r occupies
+ * ids[rec_off[r] .. rec_off[r] + rec_n1[r] + rec_n2[r]): first the side-1 ids
+ * (A), then the side-2 ids (B), original ids, each side ascending.  Records
+ * come in nondeterministic order. */
+typedef struct {
+  uint64_t cap_records, cap_ids;
+  uint64_t *rec_off;         /* [cap_records] */
+  uint32_t *rec_n1, *rec_n2; /* [cap_records] */
+  uint32_t *ids;             /* [cap_ids] */
+} mbe_output;
+
+typedef struct {
+  uint64_t count;           /* # maximal bicliques, both sides nonempty */
+  uint64_t hash;            /* Σ H(A,B) mod 2^64 over the result set */
+  uint64_t tasks;           /* search-tree nodes: popped candidates x with L' ≠ ∅ */
+  uint64_t pruned;          /* tasks rejected by the maximality check (count = tasks - pruned) */
+  uint64_t steals;          /* tasks executed by a warp other than the frame's owner */
+  uint64_t records_written; /* <= cap_records */
+  uint32_t truncated;       /* 1 if the listing overflowed (count/hash still exact) */
+  int32_t candidate_side;   /* side actually used (1 or 2) */
+  double kernel_ms;         /* device time of the search (CUDA events on the stream) */
+  double wall_ms;           /* host time of the whole call */
+  uint64_t alg_bytes;       /* MBE_STATS: algorithmic bytes */
+  uint64_t list_tasks;      /* MBE_STATS: tasks on the list (reverse-scan) path, incl. roots */
+  uint64_t bitmap_tasks;    /* MBE_STATS: tasks on the bit-row path */
+  uint64_t frames;          /* MBE_STATS: child frames pushed */
+  uint32_t n_warps;         /* persistent warps launched */
+  uint32_t max_depth;       /* MBE_STATS: deepest stack level reached */
+} mbe_result;
+
+/* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be
+ * non-NULL; out NULL = count + hash only.  Synchronous: returns when the
+ * result is on the host.  Result (count, hash) is invariant under every
+ * config field except rank/world (which select a share of the level-1
+ * subtrees; the shares of all ranks sum to the whole). */
+int mbe_enumerate(mbe_graph *g, const mbe_config *cfg, mbe_result *res, mbe_output *out);
+
+/* Static description of a loaded graph. */
+typedef struct {
+  uint32_t n1, n2;
+  uint64_t n_edges;       /* after deduplication */
+  uint32_t max_deg1, max_deg2;
+  int32_t device;
+} mbe_graph_info;
+int mbe_get_info(const mbe_graph *g, mbe_graph_info *info);
+
+void mbe_free(mbe_graph *g);             /* NULL-safe; releases host and device memory */
+const char *mbe_strerror(int code);      /* static string */
+const char *mbe_last_error_detail(void); /* thread-local message of the last failing call */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MBE_H_ */

@@ -1,0 +1,81 @@
+// mbe_internal.h — device-side data layout shared by the host driver (api.cu)
+// and the persistent search kernel (search.cu).  Product code only.
+#pragma once
+#include <stdint.h>
+
+#define MBE_MAXDEPTH 128   // per-warp stack depth (search depth is 7-11 on C2-C5)
+#define MBE_WMAX 4         // bit rows of up to 4 x 32 = 128 columns
+#define MBE_SMEM_SORT 256  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
+#define MBE_HDR_WORDS 8    // frame header
+
+// Immutable device graph after ingest.  Candidate side U is
+// relabelled by ascending (degree, original id): internal id = rank r(v).
+struct DevGraph {
+  uint32_t nU, nV;
+  uint64_t nE;
+  const uint32_t* offU;   // [nU+1]
+  const uint32_t* adjU;   // [nE]  U rank -> sorted V ids
+  const uint32_t* offV;   // [nV+1]
+  const uint32_t* adjV;   // [nE]  V id -> sorted U ranks
+  const uint64_t* hvU;    // [nU]  mix64(2*orig + side_bit(U))
+  const uint64_t* hvV;    // [nV]  mix64(2*orig + side_bit(V))
+  const uint32_t* origU;  // [nU]  rank -> original id
+  const uint32_t* root_order;  // [n_roots] execution order of level-1 tasks (cost-descending)
+  const uint8_t* twin;    // [nU] 1 if an earlier (lower-rank) vertex has exactly the same neighbourhood
+  uint32_t n_roots;
+  uint32_t maxdegU;
+};
+
+// Published frame descriptor (one per warp per depth).  claim = (nP << 32) | next.
+struct Desc {
+  unsigned long long claim;
+  unsigned int done;
+  unsigned int off;  // word offset of the frame in the owner's arena
+};
+
+struct Globals {
+  unsigned long long root_cursor;
+  unsigned int idle;
+  unsigned int error;  // 0 ok, 1 arena overflow, 2 depth overflow, 3 internal check
+  unsigned long long count, hash, tasks, pruned, steals;
+  unsigned long long list_tasks, bitmap_tasks, frames, alg_bytes;
+  unsigned int max_depth;
+  unsigned int pad;
+  unsigned long long out_records, out_ids;
+  unsigned long long err_info;
+};
+
+struct SearchParams {
+  DevGraph g;
+  int cand_side;  // 1 or 2 (A/B orientation of the hash)
+  uint32_t T;     // bitmap threshold (<= 32 * MBE_WMAX)
+  uint32_t flags;
+  uint32_t rank, world;
+  unsigned long long* claim_counter;  // NULL -> static deal
+  uint32_t n_warps;
+  // per-warp workspace: region w starts at ws + w * ws_stride (bytes); offsets below are bytes
+  uint8_t* ws;
+  uint64_t ws_stride;
+  uint64_t o_cnt, o_bits, o_tag, o_touched, o_lbuf, o_rbuf, o_skey, o_sval, o_pbuf, o_qbuf, o_arena;
+  uint64_t arena_words;
+  Desc* desc;          // [n_warps * MBE_MAXDEPTH]
+  unsigned int* tops;  // [n_warps]
+  unsigned int* stamps;  // [n_warps] persistent tag stamps
+  Globals* gl;
+  unsigned long long* per_root;  // device [nU*4] or NULL
+  // bounded listing (device buffers) or cap_records = 0
+  unsigned long long cap_records, cap_ids;
+  unsigned long long* rec_off;
+  unsigned int* rec_n1;
+  unsigned int* rec_n2;
+  unsigned int* out_ids;
+};
+
+// flags (same values as include/mbe.h)
+#define F_NO_STEAL 0x1u
+#define F_STATS 0x2u
+#define F_NO_ANTICHAIN 0x4u
+#define F_NO_TWIN 0x8u
+
+int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream);
+int mbe_search_smem_per_warp();

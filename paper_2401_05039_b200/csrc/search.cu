@@ -1,0 +1,1167 @@
+// search.cu — persistent MBEA search kernel for sm_100a.
+//
+// One WARP is one search worker ("warps = sibling tasks"): it
+// owns a LIFO stack of immutable frames in an HBM arena, claims level-1
+// subtrees (root tasks) from a global cursor, and steals single tasks from
+// other warps' frames when idle.  A task is a pair (frame F, index i): the
+// candidate x = F.P[i] with Q-role = F.Q ∪ F.P[0..i-1] and P-role =
+// F.P[i+1..] — exactly the sets Algorithm 1 holds when it pops x,
+// because it retires x into Q unconditionally and never removes
+// siblings from P.  So sibling tasks are independent and may run anywhere.
+//
+// Two task paths, chosen by |L| of the frame:
+//  * list path (root frame, and frames with |L| > T): L' = L ∩ N(x) by warp
+//    binary search; counts |N(v) ∩ L'| by REVERSE SCANNING
+//    (P:510-528): for u ∈ L', for w ∈ N(u): cnt[w]++ (warp-flattened gather,
+//    per-warp dense count table + touched list); roles by tag stamps.
+//  * bit-row path (|L| <= T <= 128): every row of P ∪ Q is a bitmask over the
+//    frame's L; L' = row(x); |N(v) ∩ L'| = popc(row(v) & row(x)); child rows
+//    are column-compressed to L' coordinates.
+// Maximality check: any Q-role v with |N(v) ∩ L'| = |L'| aborts
+// the task.  Expansion: P-role c = |L'| → R', 0 < c < |L'| → P'.
+// Children order P' by ascending (|N(v) ∩ L'|, r(v)) (iMBE).
+// Two decision-preserving reductions: Q' rows are reduced to
+// their antichain of maximal masks (R1), and among P-role siblings only an
+// identical row can be a superset (R2), checked inside the equal-key block.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bits.cuh"
+#include "mbe_internal.h"
+
+#define FULLMASK 0xffffffffu
+#define KIND_LIST 0u
+#define KIND_BITMAP 1u
+#define TAG_R 0xffffffffu
+
+namespace {
+
+struct __align__(16) WarpSmem {
+  unsigned long long skey[MBE_SMEM_SORT];
+  unsigned int sval[MBE_SMEM_SORT];
+  unsigned int hist[256];
+};
+
+struct Warp {
+  int lane;
+  uint32_t gw;
+  uint32_t* cnt;
+  uint32_t* bits;
+  unsigned long long* tag;
+  uint32_t* touched;
+  uint32_t* lbuf;
+  uint32_t* rbuf;
+  unsigned long long* skey;
+  uint32_t* sval;
+  uint32_t* pbuf;
+  uint32_t* qbuf;
+  uint32_t* arena;
+  uint64_t arena_words;
+  Desc* desc;
+  uint32_t top;
+  uint64_t atop;
+  uint32_t stamp;
+  WarpSmem* sm;
+  uint32_t cur_root;
+  // lane-0 accumulators
+  unsigned long long count, hash, tasks, pruned, steals, list_tasks, bitmap_tasks, frames, alg_bytes;
+  uint32_t max_depth;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const unsigned int* p) { return *(volatile const unsigned int*)p; }
+__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
+  return *(volatile const unsigned long long*)p;
+}
+
+__device__ __forceinline__ void set_error(const SearchParams& p, unsigned int code, unsigned long long info) {
+  if (atomicCAS(&p.gl->error, 0u, code) == 0u) p.gl->err_info = info;
+}
+
+// ------------------------------------------------------------------ rows
+template <int W>
+struct Row {
+  uint32_t w[W];
+};
+
+template <int W>
+__device__ __forceinline__ Row<W> load_row(const uint32_t* p) {
+  Row<W> r;
+  if constexpr (W == 1) {
+    r.w[0] = *p;
+  } else if constexpr (W == 2) {
+    uint2 v = *reinterpret_cast<const uint2*>(p);
+    r.w[0] = v.x;
+    r.w[1] = v.y;
+  } else {
+    uint4 v = *reinterpret_cast<const uint4*>(p);
+    r.w[0] = v.x;
+    r.w[1] = v.y;
+    r.w[2] = v.z;
+    r.w[3] = v.w;
+  }
+  return r;
+}
+
+template <int W>
+__device__ __forceinline__ void store_row(uint32_t* p, const Row<W>& r) {
+  if constexpr (W == 1) {
+    *p = r.w[0];
+  } else if constexpr (W == 2) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(r.w[0], r.w[1]);
+  } else {
+    *reinterpret_cast<uint4*>(p) = make_uint4(r.w[0], r.w[1], r.w[2], r.w[3]);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ Row<W> zero_row() {
+  Row<W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.w[k] = 0;
+  return r;
+}
+
+template <int W>
+__device__ __forceinline__ Row<W> shfl_row(const Row<W>& r, int src) {
+  Row<W> o;
+#pragma unroll
+  for (int k = 0; k < W; ++k) o.w[k] = __shfl_sync(FULLMASK, r.w[k], src);
+  return o;
+}
+
+template <int W>
+__device__ __forceinline__ bool row_subset(const Row<W>& a, const Row<W>& b) {  // a ⊆ b
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) x |= a.w[k] & ~b.w[k];
+  return x == 0;
+}
+
+template <int W>
+__device__ __forceinline__ bool row_eq(const Row<W>& a, const Row<W>& b) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) x |= a.w[k] ^ b.w[k];
+  return x == 0;
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t row_popc_and(const Row<W>& a, const Row<W>& b) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) c += __popc(a.w[k] & b.w[k]);
+  return c;
+}
+
+template <int W>
+__device__ __forceinline__ bool row_any_and(const Row<W>& a, const Row<W>& b) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) x |= a.w[k] & b.w[k];
+  return x != 0;
+}
+
+// ------------------------------------------------------------------ sorting
+// Ascending sort of n (key, val) pairs in place (keys unique: (count << 32) | id).
+__device__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, int lane) {
+  unsigned long long k = lane < (int)n ? key[lane] : ~0ull;
+  uint32_t v = lane < (int)n ? val[lane] : 0u;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      unsigned long long ok = __shfl_xor_sync(FULLMASK, k, j);
+      uint32_t ov = __shfl_xor_sync(FULLMASK, v, j);
+      bool up = (lane & size) == 0;
+      bool lower = (lane & j) == 0;
+      bool take = lower ? (up ? ok < k : ok > k) : (up ? ok > k : ok < k);
+      if (take) {
+        k = ok;
+        v = ov;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < (int)n) {
+    key[lane] = k;
+    val[lane] = v;
+  }
+  __syncwarp();
+}
+
+__device__ void sort_smem(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
+  uint32_t N = 64;
+  while (N < n) N <<= 1;
+  for (uint32_t t = lane; t < N; t += 32) {
+    sm->skey[t] = t < n ? key[t] : ~0ull;
+    sm->sval[t] = t < n ? val[t] : 0u;
+  }
+  __syncwarp();
+  for (uint32_t size = 2; size <= N; size <<= 1) {
+    for (uint32_t j = size >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = lane; t < N / 2; t += 32) {
+        uint32_t i = (t / j) * 2 * j + (t % j);
+        uint32_t l = i + j;
+        bool up = (i & size) == 0;
+        unsigned long long a = sm->skey[i], b = sm->skey[l];
+        if ((a > b) == up) {
+          sm->skey[i] = b;
+          sm->skey[l] = a;
+          uint32_t va = sm->sval[i];
+          sm->sval[i] = sm->sval[l];
+          sm->sval[l] = va;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (uint32_t t = lane; t < n; t += 32) {
+    key[t] = sm->skey[t];
+    val[t] = sm->sval[t];
+  }
+  __syncwarp();
+}
+
+// Stable LSD radix sort with 8-bit digits over the significant bits of
+// key = (count << 32) | id.  Ping-pong between (key,val) and (key2,val2).
+__device__ void sort_radix(unsigned long long* key, uint32_t* val, unsigned long long* key2, uint32_t* val2,
+                           uint32_t n, uint32_t id_bits, uint32_t cnt_bits, WarpSmem* sm, int lane) {
+  unsigned long long* src_k = key;
+  uint32_t* src_v = val;
+  unsigned long long* dst_k = key2;
+  uint32_t* dst_v = val2;
+  uint32_t shifts[8];
+  int np = 0;
+  for (uint32_t s = 0; s < id_bits; s += 8) shifts[np++] = s;
+  for (uint32_t s = 0; s < cnt_bits; s += 8) shifts[np++] = 32 + s;
+  for (int pass = 0; pass < np; ++pass) {
+    uint32_t sh = shifts[pass];
+    for (int b = lane; b < 256; b += 32) sm->hist[b] = 0;
+    __syncwarp();
+    for (uint32_t t = lane; t < n; t += 32) atomicAdd(&sm->hist[(src_k[t] >> sh) & 255u], 1u);
+    __syncwarp();
+    // exclusive scan of 256 buckets: lane owns 8 consecutive buckets
+    uint32_t loc[8];
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      loc[q] = sm->hist[lane * 8 + q];
+      s += loc[q];
+    }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t run = incl - s;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      sm->hist[lane * 8 + q] = run;
+      run += loc[q];
+    }
+    __syncwarp();
+    for (uint32_t base = 0; base < n; base += 32) {
+      uint32_t t = base + lane;
+      bool valid = t < n;
+      unsigned long long k = valid ? src_k[t] : 0ull;
+      uint32_t v = valid ? src_v[t] : 0u;
+      uint32_t d = valid ? (uint32_t)((k >> sh) & 255u) : 256u + lane;
+      uint32_t peers = __match_any_sync(FULLMASK, d);
+      uint32_t rank = __popc(peers & lanemask_lt());
+      uint32_t pos = valid ? sm->hist[d] + rank : 0u;
+      __syncwarp();
+      if (valid && rank == (uint32_t)__popc(peers) - 1u) sm->hist[d] += (uint32_t)__popc(peers);
+      if (valid) {
+        dst_k[pos] = k;
+        dst_v[pos] = v;
+      }
+      __syncwarp();
+    }
+    unsigned long long* tk = src_k;
+    src_k = dst_k;
+    dst_k = tk;
+    uint32_t* tv = src_v;
+    src_v = dst_v;
+    dst_v = tv;
+  }
+  if (src_k != key) {
+    for (uint32_t t = lane; t < n; t += 32) {
+      key[t] = src_k[t];
+      val[t] = src_v[t];
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ uint32_t bit_length(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
+
+__device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint32_t max_count) {
+  if (n <= 1) return;
+  if (n <= 32) {
+    sort_regs32(w.skey, w.sval, n, w.lane);
+  } else if (n <= MBE_SMEM_SORT) {
+    sort_smem(w.skey, w.sval, n, w.sm, w.lane);
+  } else {
+    // second buffers live right after the first ones (same per-warp region, sized nU)
+    unsigned long long* key2 = w.skey + p.g.nU;
+    uint32_t* val2 = w.sval + p.g.nU;
+    sort_radix(w.skey, w.sval, key2, val2, n, bit_length(p.g.nU), bit_length(max_count), w.sm, w.lane);
+  }
+}
+
+// ------------------------------------------------------------------ antichain (R1)
+// Reduce n candidate rows (src, W words each) to the set of distinct maximal
+// rows under inclusion, written to dst.  Decision-preserving: a later check
+// "∃q: L'' ⊆ N(q)" holds for a dominated row only if it holds for its
+// dominator.  With keep_all, rows are copied unchanged.
+template <int W>
+__device__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane) {
+  if (keep_all) {
+    for (uint32_t t = lane; t < n; t += 32) store_row<W>(dst + (size_t)t * W, load_row<W>(src + (size_t)t * W));
+    __syncwarp();
+    return n;
+  }
+  uint32_t K = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    bool valid = base + lane < n;
+    Row<W> r = valid ? load_row<W>(src + (size_t)(base + lane) * W) : zero_row<W>();
+    bool dom = !valid;
+    for (uint32_t k = 0; k < K; ++k) {
+      Row<W> kr = load_row<W>(dst + (size_t)k * W);
+      if (row_subset<W>(r, kr)) dom = true;
+    }
+    uint32_t vb = __ballot_sync(FULLMASK, valid);
+#pragma unroll 4
+    for (int m = 0; m < 32; ++m) {
+      Row<W> mr = shfl_row<W>(r, m);
+      if (((vb >> m) & 1u) && m != lane && row_subset<W>(r, mr) && (!row_eq<W>(r, mr) || m < lane)) dom = true;
+    }
+    bool surv = valid && !dom;
+    uint32_t bs = __ballot_sync(FULLMASK, surv);
+    if (bs) {
+      uint32_t newK = 0;
+      for (uint32_t kb = 0; kb < K; kb += 32) {
+        bool kval = kb + lane < K;
+        Row<W> kr = kval ? load_row<W>(dst + (size_t)(kb + lane) * W) : zero_row<W>();
+        bool kdom = false;
+        uint32_t rem = bs;
+        while (rem) {
+          int m = __ffs(rem) - 1;
+          rem &= rem - 1;
+          Row<W> sr = shfl_row<W>(r, m);
+          if (kval && row_subset<W>(kr, sr)) kdom = true;
+        }
+        bool keep = kval && !kdom;
+        uint32_t bk = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) store_row<W>(dst + (size_t)(newK + __popc(bk & lanemask_lt())) * W, kr);
+        newK += __popc(bk);
+        __syncwarp();
+      }
+      K = newK;
+      if (surv) store_row<W>(dst + (size_t)(K + __popc(bs & lanemask_lt())) * W, r);
+      K += __popc(bs);
+      __syncwarp();
+    }
+  }
+  return K;
+}
+
+__device__ __forceinline__ uint32_t antichain_w(uint32_t Wc, const uint32_t* src, uint32_t n, uint32_t* dst,
+                                                bool keep_all, int lane) {
+  if (Wc == 1) return antichain<1>(src, n, dst, keep_all, lane);
+  if (Wc == 2) return antichain<2>(src, n, dst, keep_all, lane);
+  return antichain<4>(src, n, dst, keep_all, lane);
+}
+
+// ------------------------------------------------------------------ misc
+__device__ __forceinline__ bool bsearch_u32(const uint32_t* a, uint32_t n, uint32_t v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    uint32_t x = a[mid];
+    if (x < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < n && a[lo] == v;
+}
+
+// out = A ∩ B (both sorted ascending), in ascending order; returns |out|.
+__device__ uint32_t warp_intersect(const uint32_t* A, uint32_t nA, const uint32_t* B, uint32_t nB, uint32_t* out,
+                                   int lane) {
+  if (nA > nB) {
+    const uint32_t* t = A;
+    A = B;
+    B = t;
+    uint32_t tn = nA;
+    nA = nB;
+    nB = tn;
+  }
+  uint32_t c = 0;
+  for (uint32_t base = 0; base < nA; base += 32) {
+    bool valid = base + lane < nA;
+    uint32_t v = valid ? A[base + lane] : 0u;
+    bool f = valid && bsearch_u32(B, nB, v);
+    uint32_t b = __ballot_sync(FULLMASK, f);
+    if (f) out[c + __popc(b & lanemask_lt())] = v;
+    c += __popc(b);
+  }
+  __syncwarp();
+  return c;
+}
+
+__device__ __forceinline__ uint64_t align4(uint64_t x) { return (x + 3) & ~3ull; }
+
+// Per-task accounting (tasks/pruned), lane 0.
+__device__ __forceinline__ void account_task(Warp& w, const SearchParams& p, bool pruned) {
+  if (w.lane == 0) {
+    w.tasks++;
+    if (pruned) w.pruned++;
+    if (p.per_root) {
+      atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 2], 1ull);
+      if (pruned) atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 3], 1ull);
+    }
+  }
+}
+
+__device__ __forceinline__ void account_emit(Warp& w, const SearchParams& p, uint64_t sL, uint32_t nL, uint64_t sR,
+                                             uint32_t nR) {
+  if (w.lane == 0) {
+    uint64_t h = mbe_biclique_hash(p.cand_side, sL, nL, sR, nR);
+    w.count++;
+    w.hash += h;
+    if (p.per_root) {
+      atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 0], 1ull);
+      atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 1], (unsigned long long)h);
+    }
+  }
+}
+
+// Bounded listing: record (A, B) in original ids.  Lids: L' (V ids) sorted;
+// R' = Rfr (frame R, U ranks) ∪ {x} ∪ rexp (U ranks).
+__device__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lids, uint32_t nL, const uint32_t* Rfr,
+                             uint32_t nRf, uint32_t x, const uint32_t* rexp, uint32_t nRx) {
+  uint32_t nR = nRf + 1 + nRx;
+  unsigned long long rec = 0, ido = 0;
+  if (w.lane == 0) {
+    rec = atomicAdd(&p.gl->out_records, 1ull);
+    ido = atomicAdd(&p.gl->out_ids, (unsigned long long)(nL + nR));
+  }
+  rec = __shfl_sync(FULLMASK, rec, 0);
+  ido = __shfl_sync(FULLMASK, ido, 0);
+  if (rec >= p.cap_records) return;
+  if (ido + nL + nR > p.cap_ids) {
+    if (w.lane == 0) p.rec_off[rec] = ~0ull;  // record counted but its ids did not fit
+    return;
+  }
+  uint32_t nA = p.cand_side == 1 ? nR : nL;
+  uint32_t nB = p.cand_side == 1 ? nL : nR;
+  uint32_t offR = p.cand_side == 1 ? 0u : nL;
+  uint32_t offL = p.cand_side == 1 ? nR : 0u;
+  unsigned int* ids = p.out_ids + ido;
+  for (uint32_t t = w.lane; t < nL; t += 32) ids[offL + t] = Lids[t];
+  for (uint32_t t = w.lane; t < nR; t += 32) {
+    uint32_t r = t < nRf ? Rfr[t] : (t == nRf ? x : rexp[t - nRf - 1]);
+    ids[offR + t] = p.g.origU[r];
+  }
+  if (w.lane == 0) {
+    p.rec_off[rec] = ido;
+    p.rec_n1[rec] = nA;
+    p.rec_n2[rec] = nB;
+  }
+  __syncwarp();
+}
+
+// Reserve space for a child frame at the top of the arena; false on overflow.
+__device__ __forceinline__ bool arena_reserve(Warp& w, const SearchParams& p, uint64_t words) {
+  if (w.atop + words + 8 > w.arena_words || w.top + 1 >= MBE_MAXDEPTH) {
+    if (w.lane == 0) set_error(p, w.top + 1 >= MBE_MAXDEPTH ? 2u : 1u, w.atop + words);
+    return false;
+  }
+  return true;
+}
+
+// Publish the frame just written at arena offset w.atop (size words) as depth w.top.
+__device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_words, uint32_t nP) {
+  __syncwarp();
+  if (w.lane == 0) {
+    Desc* d = &w.desc[w.top];
+    d->off = (unsigned int)w.atop;
+    d->done = 0u;
+    __threadfence();
+    atomicExch(&d->claim, ((unsigned long long)nP) << 32);
+    p.tops[w.gw] = w.top + 1;
+    w.frames++;
+  }
+  w.atop = align4(w.atop + size_words);
+  w.top += 1;
+  if (w.lane == 0 && w.top > w.max_depth) w.max_depth = w.top;
+  __syncwarp();
+}
+
+// ================================================================== list path
+// Task x on a list frame F (or the implicit root frame when F == nullptr:
+// L = V, R = ∅, Q-role = ranks < x, P-role = ranks > x).
+__device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i, uint32_t xroot) {
+  const DevGraph& g = p.g;
+  const int lane = w.lane;
+  const bool root = (F == nullptr);
+  uint32_t x, nL = 0, nP = 0, nR = 0, key = 0;
+  uint64_t sR = 0;
+  const uint32_t *L = nullptr, *R = nullptr, *Pid = nullptr;
+  if (root) {
+    x = xroot;
+  } else {
+    nL = F[1];
+    nP = F[2];
+    nR = F[4];
+    sR = *reinterpret_cast<const unsigned long long*>(F + 6);
+    L = F + MBE_HDR_WORDS;
+    R = L + nL;
+    Pid = R + nR;
+    x = Pid[i];
+    key = Pid[nP + i];
+  }
+  const uint32_t dx = g.offU[x + 1] - g.offU[x];
+  const uint32_t* Nx = g.adjU + g.offU[x];
+
+  // twin pre-pruning at the root (R2 at level 1: an earlier vertex with N(v) = N(x))
+  if (root && !(p.flags & F_NO_TWIN) && g.twin[x]) {
+    account_task(w, p, true);
+    if (lane == 0 && (p.flags & F_STATS)) w.list_tasks++;
+    return;
+  }
+
+  // Step 2: L' = L ∩ N(x)
+  const uint32_t* Lp;
+  uint32_t nLp;
+  if (root) {
+    Lp = Nx;
+    nLp = dx;
+  } else {
+    nLp = warp_intersect(L, nL, Nx, dx, w.lbuf, lane);
+    Lp = w.lbuf;
+    if (nLp != key) {
+      if (lane == 0) set_error(p, 3u, ((unsigned long long)nLp << 32) | key);
+      return;
+    }
+  }
+  if (nLp == 0) return;  // reading Z1 (only reachable for a root of degree 0, never enumerated)
+  const bool bm = nLp <= p.T;
+  const uint32_t Wc = bm ? mbe_words_for(nLp) : 0u;
+
+  // roles of frame rows: tag[v] = (stamp << 32) | (j + 1) for P[j]; TAG_R for R; untagged = Q
+  if (!root) {
+    w.stamp++;
+    const unsigned long long st = ((unsigned long long)w.stamp) << 32;
+    for (uint32_t j = lane; j < nP; j += 32) w.tag[Pid[j]] = st | (j + 1);
+    for (uint32_t j = lane; j < nR; j += 32) w.tag[R[j]] = st | TAG_R;
+    __syncwarp();
+  }
+
+  // Reverse scan: for u ∈ L' (position pos), for v ∈ N(u): cnt[v]++,
+  // bit pos of row(v) when building a bit-row child.  Flattened over the warp.
+  unsigned long long sL = 0;
+  uint32_t nt = 0;
+  unsigned long long visits = 0;
+  for (uint32_t base = 0; base < nLp; base += 32) {
+    uint32_t k = base + lane;
+    bool kv = k < nLp;
+    uint32_t u = kv ? Lp[k] : 0u;
+    uint32_t st = kv ? g.offV[u] : 0u;
+    uint32_t d = kv ? g.offV[u + 1] - st : 0u;
+    if (kv) sL += g.hvV[u];
+    uint32_t incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
+    visits += total;
+    for (uint32_t fb = 0; fb < total; fb += 32) {
+      uint32_t f = fb + lane;
+      bool fv = f < total;
+      int lo = 0;
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        uint32_t v = __shfl_sync(FULLMASK, incl, lo + s - 1);
+        if (v <= f) lo += s;
+      }
+      uint32_t o_incl = __shfl_sync(FULLMASK, incl, lo);
+      uint32_t o_d = __shfl_sync(FULLMASK, d, lo);
+      uint32_t o_st = __shfl_sync(FULLMASK, st, lo);
+      bool isnew = false;
+      uint32_t v = 0;
+      if (fv) {
+        v = g.adjV[o_st + (f - (o_incl - o_d))];
+        uint32_t old = atomicAdd(&w.cnt[v], 1u);
+        isnew = (old == 0u);
+        if (bm) {
+          uint32_t pos = base + lo;
+          atomicOr(&w.bits[(size_t)v * Wc + (pos >> 5)], 1u << (pos & 31));
+        }
+      }
+      uint32_t b = __ballot_sync(FULLMASK, isnew);
+      if (isnew) w.touched[nt + __popc(b & lanemask_lt())] = v;
+      nt += __popc(b);
+    }
+  }
+  sL = warp_sum64(sL);
+  __syncwarp();
+
+  // Classification of every touched vertex (Steps 3 and 4).
+  bool nonmax = false;
+  uint32_t nPc = 0, nQc = 0, nRx = 0;
+  unsigned long long sRx = 0;
+  for (uint32_t tb = 0; tb < nt; tb += 32) {
+    uint32_t t = tb + lane;
+    bool valid = t < nt;
+    uint32_t v = valid ? w.touched[t] : 0u;
+    uint32_t c = 0;
+    uint32_t rw[4] = {0u, 0u, 0u, 0u};
+    if (valid) {
+      c = w.cnt[v];
+      w.cnt[v] = 0u;
+      if (bm) {
+        for (uint32_t q = 0; q < Wc; ++q) {
+          rw[q] = w.bits[(size_t)v * Wc + q];
+          w.bits[(size_t)v * Wc + q] = 0u;
+        }
+      }
+    }
+    // role: 0 none/R, 1 Q-role, 2 P-role
+    int role = 0;
+    if (valid) {
+      if (root) {
+        role = v == x ? 0 : (v < x ? 1 : 2);
+      } else {
+        unsigned long long tg = w.tag[v];
+        if ((uint32_t)(tg >> 32) == w.stamp) {
+          uint32_t info = (uint32_t)tg;
+          if (info == TAG_R) role = 0;
+          else role = (info - 1 == i) ? 0 : ((info - 1 < i) ? 1 : 2);
+        } else {
+          role = 1;  // implicit Q: every vertex adjacent to L is in R ∪ P ∪ Q
+        }
+      }
+    }
+    bool isQ = role == 1;
+    bool isP = role == 2;
+    if (isQ && c == nLp) nonmax = true;
+    bool isExp = isP && c == nLp;
+    bool isPc = isP && c < nLp;
+    if (isExp) sRx += g.hvU[v];
+    uint32_t be = __ballot_sync(FULLMASK, isExp);
+    if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
+    nRx += __popc(be);
+    uint32_t bp = __ballot_sync(FULLMASK, isPc);
+    if (isPc) {
+      uint32_t idx = nPc + __popc(bp & lanemask_lt());
+      w.skey[idx] = ((unsigned long long)c << 32) | v;
+      w.sval[idx] = idx;
+      if (bm)
+        for (uint32_t q = 0; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
+    }
+    nPc += __popc(bp);
+    if (bm) {
+      uint32_t bq = __ballot_sync(FULLMASK, isQ);
+      if (isQ) {
+        uint32_t idx = nQc + __popc(bq & lanemask_lt());
+        for (uint32_t q = 0; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = rw[q];
+      }
+      nQc += __popc(bq);
+    }
+  }
+  nonmax = __any_sync(FULLMASK, nonmax);
+  sRx = warp_sum64(sRx);
+  __syncwarp();
+
+  account_task(w, p, nonmax);
+  if (lane == 0 && (p.flags & F_STATS)) {
+    w.list_tasks++;
+    // N(x) + reverse-scan adjacency incl. offsets + touched rows (+ frame L, P, R reads)
+    w.alg_bytes += 4ull * dx + 4ull * (visits + nLp) + 8ull * nt + 4ull * (nL + 2ull * nP + nR);
+  }
+  if (nonmax) return;
+
+  const uint32_t nRp = nR + 1 + nRx;
+  const uint64_t sRp = sR + g.hvU[x] + sRx;
+  account_emit(w, p, sL, nLp, sRp, nRp);
+  if (p.cap_records) write_record(w, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
+  if (nPc == 0) return;
+
+  // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.
+  warp_sort_pairs(w, p, nPc, nLp);
+  const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (bm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
+                                                            : 2ull * nPc);
+  if (!arena_reserve(w, p, need)) return;
+  uint32_t* C = w.arena + w.atop;
+  uint32_t* CL = C + MBE_HDR_WORDS;
+  uint32_t* CR = CL + nLp;
+  uint32_t* CP = CR + nRp;
+  for (uint32_t t = lane; t < nLp; t += 32) CL[t] = Lp[t];
+  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
+  uint64_t size;
+  uint32_t nQk = 0;
+  if (bm) {
+    uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
+    for (uint32_t t = lane; t < nPc; t += 32) {
+      uint32_t src = w.sval[t];
+      for (uint32_t q = 0; q < Wc; ++q) CPr[(size_t)t * Wc + q] = w.pbuf[(size_t)src * Wc + q];
+    }
+    uint32_t* CQ = CPr + (size_t)nPc * Wc;
+    __syncwarp();
+    nQk = antichain_w(Wc, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane);
+    size = (uint64_t)(CQ + (size_t)nQk * Wc - C);
+  } else {
+    uint32_t* CK = CP + nPc;
+    for (uint32_t t = lane; t < nPc; t += 32) CK[t] = (uint32_t)(w.skey[t] >> 32);
+    size = (uint64_t)(CK + nPc - C);
+  }
+  if (lane == 0) {
+    C[0] = (bm ? KIND_BITMAP : KIND_LIST) | (Wc << 8);
+    C[1] = nLp;
+    C[2] = nPc;
+    C[3] = nQk;
+    C[4] = nRp;
+    C[5] = w.cur_root;
+    *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
+    if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
+  }
+  publish_frame(w, p, size, nPc);
+}
+
+// ================================================================== bit-row path
+template <int W>
+__device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+  const DevGraph& g = p.g;
+  const int lane = w.lane;
+  const uint32_t nL = F[1], nP = F[2], nQ = F[3], nR = F[4];
+  const uint64_t sR = *reinterpret_cast<const unsigned long long*>(F + 6);
+  const uint32_t* L = F + MBE_HDR_WORDS;
+  const uint32_t* R = L + nL;
+  const uint32_t* Pid = R + nR;
+  const uint32_t* Prow = F + align4((uint64_t)(Pid + nP - F));
+  const uint32_t* Qrow = Prow + (size_t)nP * W;
+
+  const uint32_t x = Pid[i];
+  const Row<W> Lx = load_row<W>(Prow + (size_t)i * W);  // L' = row(x) (Step 2)
+  uint32_t k = 0;
+#pragma unroll
+  for (int q = 0; q < W; ++q) k += __popc(Lx.w[q]);
+
+  // Step 3, maximality.  (a) Q-role siblings P[j<i]: with ascending keys only an
+  // identical row can contain L' (R2), and identical rows share the key block.
+  bool nonmax = false;
+  for (uint32_t cb = 0; cb < i; cb += 32) {
+    int j = (int)i - 1 - (int)cb - lane;
+    bool valid = j >= 0;
+    Row<W> r = valid ? load_row<W>(Prow + (size_t)j * W) : zero_row<W>();
+    uint32_t pk = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) pk += __popc(r.w[q]);
+    if (__any_sync(FULLMASK, valid && row_eq<W>(r, Lx))) {
+      nonmax = true;
+      break;
+    }
+    if (__any_sync(FULLMASK, !valid || pk < k)) break;
+  }
+  // (b) the frame's Q rows
+  if (!nonmax) {
+    for (uint32_t qb = 0; qb < nQ; qb += 32) {
+      bool valid = qb + lane < nQ;
+      Row<W> r = valid ? load_row<W>(Qrow + (size_t)(qb + lane) * W) : zero_row<W>();
+      if (__any_sync(FULLMASK, valid && row_subset<W>(Lx, r))) {
+        nonmax = true;
+        break;
+      }
+    }
+  }
+  account_task(w, p, nonmax);
+  if (lane == 0 && (p.flags & F_STATS)) {
+    w.bitmap_tasks++;
+    w.alg_bytes += 4ull * W * (1ull + nP + nQ) + 4ull * nP;
+  }
+  if (nonmax) return;
+
+  // Step 4, expansion over P-role rows j > i.
+  const uint32_t Wn = mbe_words_for(k);
+  const MbeCompress<W> cmp = mbe_compress_prep_w<W>(Lx.w);
+  uint32_t nPc = 0, nRx = 0, nQc = 0;
+  unsigned long long sRx = 0;
+  for (uint32_t jb = i + 1; jb < nP; jb += 32) {
+    uint32_t j = jb + lane;
+    bool valid = j < nP;
+    Row<W> r = valid ? load_row<W>(Prow + (size_t)j * W) : zero_row<W>();
+    uint32_t c = row_popc_and<W>(r, Lx);
+    uint32_t v = valid ? Pid[j] : 0u;
+    bool isExp = valid && c == k;
+    bool isPc = valid && c > 0 && c < k;
+    if (isExp) sRx += g.hvU[v];
+    uint32_t be = __ballot_sync(FULLMASK, isExp);
+    if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
+    nRx += __popc(be);
+    uint32_t bp = __ballot_sync(FULLMASK, isPc);
+    if (isPc) {
+      uint32_t idx = nPc + __popc(bp & lanemask_lt());
+      w.skey[idx] = ((unsigned long long)c << 32) | v;
+      w.sval[idx] = idx;
+      uint32_t out[4];
+      mbe_compress_apply_w<W>(cmp, r.w, out);
+      for (uint32_t q = 0; q < Wn; ++q) w.pbuf[(size_t)idx * Wn + q] = out[q];
+    }
+    nPc += __popc(bp);
+  }
+  sRx = warp_sum64(sRx);
+  // sum of hv over L' = L[positions of set bits of row(x)]
+  unsigned long long sL = 0;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    uint32_t pos = q * 32 + lane;
+    if ((Lx.w[q] >> lane) & 1u) sL += g.hvV[L[pos]];
+  }
+  sL = warp_sum64(sL);
+  const uint32_t nRp = nR + 1 + nRx;
+  const uint64_t sRp = sR + g.hvU[x] + sRx;
+  account_emit(w, p, sL, k, sRp, nRp);
+
+  const bool need_child = nPc > 0;
+  if (!need_child && !p.cap_records) return;
+
+  // L' ids in ascending order (L is sorted, positions ascending): into lbuf
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    uint32_t bit = (Lx.w[q] >> lane) & 1u;
+    uint32_t b = Lx.w[q];
+    uint32_t before = 0;
+    for (int qq = 0; qq < q; ++qq) before += __popc(Lx.w[qq]);
+    if (bit) w.lbuf[before + __popc(b & lanemask_lt())] = L[q * 32 + lane];
+  }
+  __syncwarp();
+  if (p.cap_records) write_record(w, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
+  if (!need_child) return;
+
+  // Q' candidates: frame Q rows and Q-role siblings P[j<i] meeting L'
+  for (uint32_t qb = 0; qb < nQ + i; qb += 32) {
+    uint32_t t = qb + lane;
+    bool valid = t < nQ + i;
+    Row<W> r = zero_row<W>();
+    if (valid) r = t < nQ ? load_row<W>(Qrow + (size_t)t * W) : load_row<W>(Prow + (size_t)(t - nQ) * W);
+    bool keep = valid && row_any_and<W>(r, Lx);
+    uint32_t bq = __ballot_sync(FULLMASK, keep);
+    if (keep) {
+      uint32_t idx = nQc + __popc(bq & lanemask_lt());
+      uint32_t out[4];
+      mbe_compress_apply_w<W>(cmp, r.w, out);
+      for (uint32_t q = 0; q < Wn; ++q) w.qbuf[(size_t)idx * Wn + q] = out[q];
+    }
+    nQc += __popc(bq);
+  }
+  __syncwarp();
+  warp_sort_pairs(w, p, nPc, k);
+
+  const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (1 + Wn) + (uint64_t)nQc * Wn;
+  if (!arena_reserve(w, p, need)) return;
+  uint32_t* C = w.arena + w.atop;
+  uint32_t* CL = C + MBE_HDR_WORDS;
+  uint32_t* CR = CL + k;
+  uint32_t* CP = CR + nRp;
+  for (uint32_t t = lane; t < k; t += 32) CL[t] = w.lbuf[t];
+  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
+  uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
+  for (uint32_t t = lane; t < nPc; t += 32) {
+    uint32_t src = w.sval[t];
+    for (uint32_t q = 0; q < Wn; ++q) CPr[(size_t)t * Wn + q] = w.pbuf[(size_t)src * Wn + q];
+  }
+  uint32_t* CQ = CPr + (size_t)nPc * Wn;
+  __syncwarp();
+  uint32_t nQk = antichain_w(Wn, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane);
+  uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
+  if (lane == 0) {
+    C[0] = KIND_BITMAP | (Wn << 8);
+    C[1] = k;
+    C[2] = nPc;
+    C[3] = nQk;
+    C[4] = nRp;
+    C[5] = w.cur_root;
+    *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
+    if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
+  }
+  publish_frame(w, p, size, nPc);
+}
+
+__device__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+  const uint32_t h = F[0];
+  w.cur_root = F[5];
+  if ((h & 0xffu) == KIND_LIST) {
+    list_task(w, p, F, i, 0u);
+  } else {
+    const uint32_t W = (h >> 8) & 0xffu;
+    if (W == 1) bitmap_task<1>(w, p, F, i);
+    else if (W == 2) bitmap_task<2>(w, p, F, i);
+    else bitmap_task<4>(w, p, F, i);
+  }
+}
+
+// ================================================================== kernel
+__global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (gw >= p.n_warps) return;
+
+  Warp w;
+  w.lane = lane;
+  w.gw = gw;
+  uint8_t* base = p.ws + (size_t)gw * p.ws_stride;
+  w.cnt = reinterpret_cast<uint32_t*>(base + p.o_cnt);
+  w.bits = reinterpret_cast<uint32_t*>(base + p.o_bits);
+  w.tag = reinterpret_cast<unsigned long long*>(base + p.o_tag);
+  w.touched = reinterpret_cast<uint32_t*>(base + p.o_touched);
+  w.lbuf = reinterpret_cast<uint32_t*>(base + p.o_lbuf);
+  w.rbuf = reinterpret_cast<uint32_t*>(base + p.o_rbuf);
+  w.skey = reinterpret_cast<unsigned long long*>(base + p.o_skey);
+  w.sval = reinterpret_cast<uint32_t*>(base + p.o_sval);
+  w.pbuf = reinterpret_cast<uint32_t*>(base + p.o_pbuf);
+  w.qbuf = reinterpret_cast<uint32_t*>(base + p.o_qbuf);
+  w.arena = reinterpret_cast<uint32_t*>(base + p.o_arena);
+  w.arena_words = p.arena_words;
+  w.desc = p.desc + (size_t)gw * MBE_MAXDEPTH;
+  w.top = 0;
+  w.atop = 0;
+  w.stamp = p.stamps[gw];
+  w.sm = reinterpret_cast<WarpSmem*>(smem_raw) + wib;
+  w.cur_root = 0;
+  w.count = w.hash = w.tasks = w.pruned = w.steals = 0;
+  w.list_tasks = w.bitmap_tasks = w.frames = w.alg_bytes = 0;
+  w.max_depth = 0;
+
+  const bool steal = !(p.flags & F_NO_STEAL);
+  bool roots_done = false;
+  bool registered = false;
+  uint32_t backoff = 32;
+
+  while (true) {
+    uint32_t err = 0;
+    if (lane == 0) err = ld_volatile(&p.gl->error);
+    if (__shfl_sync(FULLMASK, err, 0)) break;
+    if (w.top > 0) {
+      Desc* d = &w.desc[w.top - 1];
+      unsigned long long old = 0;
+      if (lane == 0) old = atomicAdd(&d->claim, 1ull);
+      old = __shfl_sync(FULLMASK, old, 0);
+      const uint32_t nP = (uint32_t)(old >> 32), i = (uint32_t)old;
+      if (i < nP) {
+        const uint32_t* F = w.arena + d->off;
+        run_task(w, p, F, i);
+        __syncwarp();
+        if (lane == 0) atomicAdd(&d->done, 1u);
+      } else {
+        if (lane == 0) {
+          while (ld_volatile(&d->done) < nP && !ld_volatile(&p.gl->error)) __nanosleep(64);
+          atomicExch(&d->claim, 0ull);
+          d->done = 0u;
+        }
+        const uint32_t off = d->off;
+        __syncwarp();
+        w.top -= 1;
+        w.atop = off;
+        if (lane == 0) p.tops[gw] = w.top;
+      }
+      continue;
+    }
+    // empty stack: next level-1 subtree (coarse-grained task)
+    if (!roots_done) {
+      unsigned long long pos = 0;
+      if (lane == 0) {
+        if (p.claim_counter) pos = atomicAdd(p.claim_counter, 1ull);
+        else pos = atomicAdd(&p.gl->root_cursor, 1ull) * p.world + p.rank;
+      }
+      pos = __shfl_sync(FULLMASK, pos, 0);
+      if (pos < p.g.n_roots) {
+        const uint32_t x = p.g.root_order[pos];
+        w.cur_root = x;
+        list_task(w, p, nullptr, 0u, x);
+        continue;
+      }
+      roots_done = true;
+    }
+    // idle: register, then steal single tasks or terminate (SURVEY §7.2 termination)
+    if (!registered) {
+      if (lane == 0) atomicAdd(&p.gl->idle, 1u);
+      registered = true;
+    }
+    uint32_t stop = 0;
+    if (lane == 0) stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
+    if (__shfl_sync(FULLMASK, stop, 0)) break;
+    if (!steal) {
+      __nanosleep(256);
+      continue;
+    }
+    // scan victims circularly from gw+1 (as P:430-431); each lane probes one victim
+    int fv = -1, fd = -1;
+    for (uint32_t vb = 0; vb + 1 < p.n_warps && fv < 0; vb += 32) {
+      uint32_t t = vb + lane;
+      int myd = -1;
+      uint32_t v = (gw + 1 + t) % p.n_warps;
+      if (t + 1 < p.n_warps) {
+        uint32_t tp = ld_volatile(&p.tops[v]);
+        const Desc* vd = p.desc + (size_t)v * MBE_MAXDEPTH;
+        for (uint32_t dd = 0; dd < tp && dd < MBE_MAXDEPTH; ++dd) {
+          unsigned long long c = ld_volatile64(&vd[dd].claim);
+          if ((uint32_t)c < (uint32_t)(c >> 32)) {
+            myd = (int)dd;
+            break;
+          }
+        }
+      }
+      uint32_t b = __ballot_sync(FULLMASK, myd >= 0);
+      if (b) {
+        int src = __ffs(b) - 1;
+        fv = __shfl_sync(FULLMASK, (int)v, src);
+        fd = __shfl_sync(FULLMASK, myd, src);
+      }
+    }
+    if (fv < 0) {
+      __nanosleep(backoff);
+      if (backoff < 4096) backoff <<= 1;
+      continue;
+    }
+    backoff = 32;
+    Desc* vd = p.desc + (size_t)fv * MBE_MAXDEPTH + fd;
+    unsigned long long old = 0;
+    if (lane == 0) {
+      atomicSub(&p.gl->idle, 1u);
+      old = atomicAdd(&vd->claim, 1ull);
+      if ((uint32_t)old >= (uint32_t)(old >> 32)) atomicAdd(&p.gl->idle, 1u);
+    }
+    old = __shfl_sync(FULLMASK, old, 0);
+    if ((uint32_t)old >= (uint32_t)(old >> 32)) continue;  // lost the race; still registered idle
+    registered = false;
+    __threadfence();  // acquire: the victim published the frame before the claim word
+    const uint32_t off = ld_volatile(&vd->off);
+    const uint32_t* F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)fv * p.ws_stride + p.o_arena) + off;
+    run_task(w, p, F, (uint32_t)old);
+    __syncwarp();
+    if (lane == 0) {
+      w.steals++;
+      atomicAdd(&vd->done, 1u);
+    }
+  }
+
+  // flush lane-0 accumulators
+  if (lane == 0) {
+    p.stamps[gw] = w.stamp;
+    atomicAdd(&p.gl->count, w.count);
+    atomicAdd(&p.gl->hash, w.hash);
+    atomicAdd(&p.gl->tasks, w.tasks);
+    atomicAdd(&p.gl->pruned, w.pruned);
+    atomicAdd(&p.gl->steals, w.steals);
+    if (p.flags & F_STATS) {
+      atomicAdd(&p.gl->list_tasks, w.list_tasks);
+      atomicAdd(&p.gl->bitmap_tasks, w.bitmap_tasks);
+      atomicAdd(&p.gl->frames, w.frames);
+      atomicAdd(&p.gl->alg_bytes, w.alg_bytes);
+      atomicMax(&p.gl->max_depth, w.max_depth);
+    }
+  }
+}
+
+// Twin flags for level-1 pruning (R2 at the root): twin[x] = 1
+// iff some vertex of lower rank has exactly N(x).  Lower rank and N(v) ⊇ N(x)
+// force equality since deg(v) <= deg(x).  One warp per vertex: candidates are
+// the vertices of rank < x and equal degree adjacent to x's lowest-degree
+// neighbour u; each is compared element-wise.
+__global__ void __launch_bounds__(256) mbe_twin_kernel(DevGraph g, uint8_t* twin) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; x < g.nU; x += nwarps) {
+    const uint32_t ox = g.offU[x], dx = g.offU[x + 1] - ox;
+    uint32_t res = 0;
+    if (dx > 0) {
+      // lowest-degree neighbour of x
+      uint32_t best_d = 0xffffffffu, best_u = 0;
+      for (uint32_t t = lane; t < dx; t += 32) {
+        uint32_t u = g.adjU[ox + t];
+        uint32_t du = g.offV[u + 1] - g.offV[u];
+        if (du < best_d || (du == best_d && u < best_u)) {
+          best_d = du;
+          best_u = u;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        uint32_t od = __shfl_xor_sync(FULLMASK, best_d, o), ou = __shfl_xor_sync(FULLMASK, best_u, o);
+        if (od < best_d || (od == best_d && ou < best_u)) {
+          best_d = od;
+          best_u = ou;
+        }
+      }
+      // first rank with degree dx: lower_bound over the non-decreasing degrees
+      uint32_t lo = 0, hi = x;
+      while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (g.offU[mid + 1] - g.offU[mid] < dx) lo = mid + 1;
+        else hi = mid;
+      }
+      const uint32_t rlo = lo;
+      const uint32_t* Nu = g.adjV + g.offV[best_u];
+      // candidates v in N(u) with rlo <= v < x
+      uint32_t a = 0, b = best_d;
+      while (a < b) {
+        uint32_t mid = (a + b) >> 1;
+        if (Nu[mid] < rlo) a = mid + 1;
+        else b = mid;
+      }
+      for (uint32_t c = a; c < best_d && !res; ++c) {
+        uint32_t v = Nu[c];
+        if (v >= x) break;
+        const uint32_t* Nv = g.adjU + g.offU[v];
+        bool diff = false;
+        for (uint32_t t = lane; t < dx; t += 32)
+          if (Nv[t] != g.adjU[ox + t]) diff = true;
+        if (!__any_sync(FULLMASK, diff)) res = 1;
+      }
+    }
+    if (lane == 0) twin[x] = (uint8_t)res;
+  }
+}
+
+}  // namespace
+
+int mbe_search_smem_per_warp() { return (int)sizeof(WarpSmem); }
+
+int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!(p.flags & F_NO_TWIN)) {
+    mbe_twin_kernel<<<148 * 8, 256, 0, s>>>(p.g, const_cast<uint8_t*>(p.g.twin));
+    if (cudaGetLastError() != cudaSuccess) return -1;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(mbe_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+        cudaSuccess)
+      return -1;
+    attr_set = true;
+  }
+  mbe_search_kernel<<<grid, block, smem_bytes, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}

@@ -1,0 +1,251 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Integer work: every comparison is bit-exact — count, 64-bit hash, and, because
+both sides use the same candidate order (reading Z6), the search-tree task
+and pruned counts.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import reference as R
+from paper_2401_05039_b200 import MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN, MBE_STATS, MBEGraph
+from paper_2401_05039_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2401_05039_b200 import build
+
+    build.build()
+
+
+def gpu(g, **cfg):
+    with MBEGraph.from_graph(g) as G:
+        return G.enumerate(**cfg)
+
+
+def same(res, want):
+    return (res.count, res.hash, res.tasks, res.pruned) == (want.count, want.hash, want.tasks, want.pruned)
+
+
+def _random_graphs(n_graphs, max_side, seed0):
+    ps = [0.1, 0.3, 0.5, 0.7, 0.9]
+    for k in range(n_graphs):
+        z = R.mix64(seed0 + k)
+        yield I.random_bipartite(1 + z % max_side, 1 + (z >> 8) % max_side, ps[k % 5], seed0 * 1000 + k)
+
+
+# ------------------------------------------------------------------ closed forms and C1
+@pytest.mark.parametrize("g", [I.crown(2), I.crown(5), I.crown(12), I.complete(1, 1), I.complete(3, 7),
+                               I.complete(40, 33), I.perfect_matching(9), I.path(9), I.star(50),
+                               I.disjoint_blocks([(2, 3), (1, 1), (4, 2), (3, 3)])], ids=lambda g: g.name)
+def test_closed_forms(g):
+    assert same(gpu(g), oracle.mbea(g))
+
+
+def test_empty_graphs():
+    for n1, n2 in [(0, 0), (0, 5), (4, 0), (5, 7)]:
+        r = gpu(I.from_edges(n1, n2, [], []))
+        assert (r.count, r.hash, r.tasks) == (0, 0, 0)
+
+
+def test_c1_golden():
+    r = gpu(I.crown(12))
+    assert (r.count, r.hash) == (4094, 0x8B42CB5CE2038215)
+    g = I.erdos_renyi_c1b()
+    r = gpu(g)
+    assert (r.count, r.hash) == (1837, 0xD71911BE703AC684)
+    assert same(r, oracle.mbea(g))
+
+
+# ------------------------------------------------------------------ random graphs
+def test_random_small_graphs_individually():
+    for g in _random_graphs(300, 12, 101):
+        assert same(gpu(g), oracle.mbea(g)), g.name
+
+
+def test_random_disjoint_union_of_1000_graphs():
+    """1,000 random graphs (sides <= 10, p 0.1-0.9) as one disjoint union: bicliques cannot span
+    components, so count and hash are sums; checked against the oracle on the same union."""
+    rows, cols, o1, o2 = [], [], 0, 0
+    for g in _random_graphs(1000, 10, 202):
+        e = g.edges()
+        rows.append(e[:, 0].astype(np.int64) + o1)
+        cols.append(e[:, 1].astype(np.int64) + o2)
+        o1 += g.n1
+        o2 += g.n2
+    u = I.from_edges(o1, o2, np.concatenate(rows), np.concatenate(cols))
+    assert same(gpu(u), oracle.mbea(u))
+
+
+@pytest.mark.parametrize("n,p", [(60, 0.3), (120, 0.15), (300, 0.03), (64, 0.6)])
+def test_random_mid_graphs_both_sides(n, p):
+    g = I.random_bipartite(n, n + 17, p, 77 + n)
+    for side in (1, 2):
+        assert same(gpu(g, candidate_side=side), oracle.mbea(g, candidate_side=side))
+
+
+# ------------------------------------------------------------------ result invariance under every knob
+@pytest.mark.parametrize("T", [32, 64, 128])
+@pytest.mark.parametrize("flags", [0, MBE_NO_STEAL, MBE_NO_ANTICHAIN | MBE_NO_TWIN, MBE_STATS])
+def test_knobs_do_not_change_result_or_tree(T, flags):
+    g = I.erdos_renyi_c1b()
+    want = oracle.mbea(g)
+    assert same(gpu(g, bitmap_threshold=T, flags=flags), want)
+
+
+@pytest.mark.parametrize("ctas,threads", [(1, 32), (1, 256), (2, 128), (4, 64)])
+def test_launch_shapes(ctas, threads):
+    g = I.random_bipartite(200, 150, 0.06, 5)
+    assert same(gpu(g, ctas_per_sm=ctas, threads_per_cta=threads), oracle.mbea(g))
+
+
+def test_small_arena_grows_or_reports_overflow():
+    g = I.random_bipartite(200, 150, 0.08, 6)
+    want = oracle.mbea(g)
+    from paper_2401_05039_b200 import MBEError
+
+    try:
+        r = gpu(g, arena_bytes=4096)
+        assert same(r, want)  # fits
+    except MBEError as e:
+        assert e.code == -4  # MBE_EOVERFLOW, never a silently wrong count
+    assert same(gpu(g), want)  # auto arena
+
+
+# ------------------------------------------------------------------ listing
+def test_listing_equals_oracle_set():
+    for g in list(_random_graphs(60, 14, 303)) + [I.crown(7), I.erdos_renyi_c1b(80, 60)]:
+        with MBEGraph.from_graph(g) as G:
+            r, recs = G.enumerate_list()
+        assert len(recs) == r.count and not r.truncated
+        assert len(set(recs)) == len(recs), "duplicate emission"
+        assert set(recs) == set(oracle.mbea_list(g))
+
+
+def test_listing_truncates_but_counts_stay_exact():
+    g = I.crown(9)
+    with MBEGraph.from_graph(g) as G:
+        r, recs = G.enumerate_list(cap_records=10, cap_ids=1 << 12)
+    assert r.count == 510 and r.truncated and len(recs) <= 10
+    fam = {(tuple(i for i in range(9) if S >> i & 1), tuple(j for j in range(9) if not S >> j & 1))
+           for S in range(1, 511)}
+    assert set(recs) <= fam
+
+
+# ------------------------------------------------------------------ metamorphic
+def test_metamorphic_transpose_isolated_duplicates():
+    g = I.erdos_renyi_c1b(150, 90)
+    base = gpu(g)
+    gt = g.transpose()
+    want_t = oracle.mbea(gt)
+    assert same(gpu(gt), want_t) and want_t.count == base.count
+    e = g.edges()
+    gi = I.from_edges(g.n1 + 9, g.n2 + 4, e[:, 0], e[:, 1])
+    assert (gpu(gi).count, gpu(gi).hash) == (base.count, base.hash)
+    gd = I.from_edges(g.n1, g.n2, np.concatenate([e[:, 0], e[:50, 0]]), np.concatenate([e[:, 1], e[:50, 1]]),
+                      dedup=False)
+    assert (gpu(gd).count, gpu(gd).hash) == (base.count, base.hash)
+
+
+# ------------------------------------------------------------------ per-root parity and multi-rank shares
+def test_per_root_sums_and_values_c1b():
+    g = I.erdos_renyi_c1b()
+    for side in (1, 2):
+        with MBEGraph.from_graph(g) as G:
+            r, pr = G.enumerate_per_root(candidate_side=side)
+        want = oracle.mbea_roots(g, np.arange(g.n1 if side == 1 else g.n2), candidate_side=side)
+        assert np.array_equal(pr, want)
+        assert int(pr[:, 0].sum()) == r.count
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_rank_shares_sum_to_whole(world):
+    g = I.random_bipartite(300, 250, 0.04, 9)
+    want = oracle.mbea(g)
+    tot = [0, 0, 0, 0]
+    with MBEGraph.from_graph(g) as G:
+        for rank in range(world):
+            r = G.enumerate(rank=rank, world=world)
+            tot[0] += r.count
+            tot[1] = (tot[1] + r.hash) & R.MASK64
+            tot[2] += r.tasks
+            tot[3] += r.pruned
+    assert tot == [want.count, want.hash, want.tasks, want.pruned]
+
+
+def test_shared_claim_counter_logical_ranks():
+    """Dynamic claiming through one device counter shared by 2 logical ranks (one GPU)."""
+    import threading
+
+    import torch
+
+    g = I.random_bipartite(400, 300, 0.03, 10)
+    want = oracle.mbea(g)
+    ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+    Gs = [MBEGraph.from_graph(g) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    out = [None, None]
+
+    def run(k):
+        out[k] = Gs[k].enumerate(rank=k, world=2, claim_counter=ctr.data_ptr(), stream=streams[k].cuda_stream)
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for G in Gs:
+        G.close()
+    assert out[0].count + out[1].count == want.count
+    assert (out[0].hash + out[1].hash) & R.MASK64 == want.hash
+    assert out[0].tasks + out[1].tasks == want.tasks
+
+
+# ------------------------------------------------------------------ full-size configs
+def _golden_configs():
+    path = os.path.join(GOLD, "configs.txt")
+    rows = {}
+    if os.path.exists(path):
+        for line in open(path):
+            if line.strip() and not line.startswith("#"):
+                name, cnt, h, tasks, pruned = line.split()[:5]
+                rows[name] = (int(cnt), int(h, 16), int(tasks), int(pruned))
+    return rows
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_full_config_matches_oracle_golden(cfg):
+    gold = _golden_configs()
+    if cfg not in gold:
+        pytest.skip(f"no oracle golden for {cfg} (scripts/make_golden.py)")
+    g = I.config_graph(cfg)
+    r = gpu(g)
+    assert (r.count, r.hash, r.tasks, r.pruned) == gold[cfg]
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_full_config_sampled_roots_vs_oracle(cfg):
+    """At full size, in the bench launch configuration: per level-1 subtree results for a seeded
+    sample of roots (the heaviest by degree plus uniform ones) equal the oracle's, computed one by one."""
+    g = I.config_graph(cfg)
+    side = 2 if g.n2 < g.n1 else 1
+    n = g.n1 if side == 1 else g.n2
+    deg = np.bincount(g.col_idx, minlength=g.n2) if side == 2 else np.diff(g.row_ptr.astype(np.int64))
+    rng = np.random.default_rng(2024)
+    sample = np.unique(np.concatenate([np.argsort(-deg, kind="stable")[:8], rng.choice(n, 120, replace=False)]))
+    with MBEGraph.from_graph(g) as G:
+        r, pr = G.enumerate_per_root(candidate_side=side)
+    want = oracle.mbea_roots(g, sample, candidate_side=side)
+    assert np.array_equal(pr[sample], want)
+    assert int(pr[:, 0].sum()) == r.count
+    assert int(pr[:, 2].sum()) == r.tasks
