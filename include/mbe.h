@@ -108,6 +108,11 @@ typedef struct {
   uint64_t frames;          /* MBE_STATS: child frames pushed */
   uint32_t n_warps;         /* persistent warps launched */
   uint32_t max_depth;       /* MBE_STATS: deepest stack level reached */
+  /* MBE_STATS: Σ over warps of SM cycles spent per phase (the Eq. 1 breakdown, and the
+   * fetch/steal/idle shares of Fig. 6): [0] level-1 (root) tasks incl. subtree fetch,
+   * [1] list-path tasks, [2] bit-row tasks, [3] stealing (scan + claim), [4] idle backoff,
+   * [5] waiting for thieves before a pop, [6..7] reserved. */
+  uint64_t phase_cycles[8];
 } mbe_result;
 
 /* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be

@@ -44,7 +44,7 @@ class mbe_result(ctypes.Structure):
     _fields_ = [("count", _u64), ("hash", _u64), ("tasks", _u64), ("pruned", _u64), ("steals", _u64),
                 ("records_written", _u64), ("truncated", _u32), ("candidate_side", _i32), ("kernel_ms", _dbl),
                 ("wall_ms", _dbl), ("alg_bytes", _u64), ("list_tasks", _u64), ("bitmap_tasks", _u64),
-                ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32)]
+                ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 8)]
 
 
 class mbe_graph_info(ctypes.Structure):
@@ -110,6 +110,7 @@ class Result:
     max_depth: int
     records_written: int = 0
     truncated: bool = False
+    phase_cycles: tuple = ()
 
 
 def mbe_strerror(code: int) -> str:
@@ -164,7 +165,8 @@ def mbe_enumerate(handle: int, config: Optional[mbe_config] = None, output: Opti
     return Result(int(res.count), int(res.hash), int(res.tasks), int(res.pruned), int(res.steals),
                   int(res.candidate_side), float(res.kernel_ms), float(res.wall_ms), int(res.alg_bytes),
                   int(res.list_tasks), int(res.bitmap_tasks), int(res.frames), int(res.n_warps),
-                  int(res.max_depth), int(res.records_written), bool(res.truncated))
+                  int(res.max_depth), int(res.records_written), bool(res.truncated),
+                  tuple(int(v) for v in res.phase_cycles))
 
 
 def mbe_get_info(handle: int) -> dict:

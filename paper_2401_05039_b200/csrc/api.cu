@@ -78,7 +78,7 @@ struct mbe_graph {
   std::vector<uint32_t> off1, adj1, off2, adj2;
   Side side[2];
   // workspace cache
-  DevBuf ws, desc, tops, stamps, gl, per_root;
+  DevBuf ws, desc, tops, stamps, hint, gl, per_root;
   uint64_t ws_stride = 0, arena_bytes = 0;
   uint32_t ws_warps = 0, ws_side = 0, ws_wmax = 0;
   bool ws_dirty = true;
@@ -87,7 +87,7 @@ struct mbe_graph {
   int sm_count = 0;
   ~mbe_graph() {
     for (auto& s : side) s.release();
-    for (DevBuf* b : {&ws, &desc, &tops, &stamps, &gl, &per_root}) b->release();
+    for (DevBuf* b : {&ws, &desc, &tops, &stamps, &hint, &gl, &per_root}) b->release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
   }
@@ -182,13 +182,11 @@ int ensure_workspace(mbe_graph* g, int s, uint32_t n_warps, uint64_t arena_bytes
       g->ws_wmax == wmax) {
     return MBE_OK;
   }
-  for (DevBuf* b : {&g->ws, &g->desc, &g->tops, &g->stamps, &g->per_root}) b->release();
+  for (DevBuf* b : {&g->ws, &g->desc, &g->tops, &g->stamps, &g->hint, &g->per_root}) b->release();
   const uint64_t nU = std::max<uint32_t>(S.nU, 1);
   SearchParams& p = g->sp;
   uint64_t o = 0;
-  p.o_cnt = o; o = align256(o + nU * 4);
-  p.o_bits = o; o = align256(o + nU * wmax * 4);
-  p.o_tag = o; o = align256(o + nU * 8);
+  p.o_slot = o; o = align256(o + nU * 32);
   p.o_touched = o; o = align256(o + nU * 4);
   p.o_lbuf = o; o = align256(o + (uint64_t)std::max<uint32_t>(S.maxdegU, 32 * MBE_WMAX) * 4);
   p.o_rbuf = o; o = align256(o + nU * 4);
@@ -207,6 +205,7 @@ int ensure_workspace(mbe_graph* g, int s, uint32_t n_warps, uint64_t arena_bytes
   g->ws.bytes = total;
   if (cudaMalloc(&g->desc.p, sizeof(Desc) * MBE_MAXDEPTH * n_warps) != cudaSuccess ||
       cudaMalloc(&g->tops.p, 4ull * n_warps) != cudaSuccess || cudaMalloc(&g->stamps.p, 4ull * n_warps) != cudaSuccess ||
+      cudaMalloc(&g->hint.p, 4ull * ((n_warps + 31) / 32)) != cudaSuccess ||
       cudaMalloc(&g->per_root.p, 32ull * nU) != cudaSuccess) {
     cudaGetLastError();
     return fail(MBE_ENOMEM, "workspace descriptors");
@@ -223,8 +222,8 @@ int ensure_workspace(mbe_graph* g, int s, uint32_t n_warps, uint64_t arena_bytes
 // zero the per-warp cnt/bits/tag tables (required invariant: zero between tasks)
 int clear_tables(mbe_graph* g, cudaStream_t st) {
   const SearchParams& p = g->sp;
-  // cnt, bits and tag are contiguous from o_cnt to o_touched
-  CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(g->ws.p) + p.o_cnt, g->ws_stride, 0, p.o_touched - p.o_cnt,
+  // per-vertex slots (count, tag, bit row) must be zero between tasks
+  CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(g->ws.p) + p.o_slot, g->ws_stride, 0, p.o_touched - p.o_slot,
                              g->ws_warps, st));
   CUDA_TRY(cudaMemsetAsync(g->stamps.p, 0, 4ull * g->ws_warps, st));
   g->ws_dirty = false;
@@ -430,6 +429,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.desc = static_cast<Desc*>(g->desc.p);
     p.tops = static_cast<unsigned int*>(g->tops.p);
     p.stamps = static_cast<unsigned int*>(g->stamps.p);
+    p.hint = static_cast<unsigned int*>(g->hint.p);
     p.gl = static_cast<Globals*>(g->gl.p);
     p.per_root = cfg.per_root ? static_cast<unsigned long long*>(g->per_root.p) : nullptr;
     p.cap_records = cap_rec;
@@ -442,6 +442,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     CUDA_TRY(cudaMemsetAsync(g->gl.p, 0, sizeof(Globals), st));
     CUDA_TRY(cudaMemsetAsync(g->desc.p, 0, sizeof(Desc) * MBE_MAXDEPTH * n_warps, st));
     CUDA_TRY(cudaMemsetAsync(g->tops.p, 0, 4ull * n_warps, st));
+    CUDA_TRY(cudaMemsetAsync(g->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
     if (p.per_root) CUDA_TRY(cudaMemsetAsync(g->per_root.p, 0, 32ull * S.nU, st));
     const int smem = mbe_search_smem_per_warp() * (int)(threads / 32);
     CUDA_TRY(cudaEventRecord(g->ev0, st));
@@ -481,6 +482,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     res->frames = hg.frames;
     res->n_warps = n_warps;
     res->max_depth = hg.max_depth;
+    for (int k = 0; k < 8; ++k) res->phase_cycles[k] = hg.phase[k];
     if (cfg.per_root) {
       std::vector<uint64_t> pr(4ull * S.nU);
       CUDA_TRY(cudaMemcpy(pr.data(), g->per_root.p, 32ull * S.nU, cudaMemcpyDeviceToHost));

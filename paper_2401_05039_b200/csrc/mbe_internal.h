@@ -43,6 +43,7 @@ struct Globals {
   unsigned int pad;
   unsigned long long out_records, out_ids;
   unsigned long long err_info;
+  unsigned long long phase[8];  // MBE_STATS: Σ over warps of cycles per phase (see mbe.h)
 };
 
 struct SearchParams {
@@ -56,11 +57,12 @@ struct SearchParams {
   // per-warp workspace: region w starts at ws + w * ws_stride (bytes); offsets below are bytes
   uint8_t* ws;
   uint64_t ws_stride;
-  uint64_t o_cnt, o_bits, o_tag, o_touched, o_lbuf, o_rbuf, o_skey, o_sval, o_pbuf, o_qbuf, o_arena;
+  uint64_t o_slot, o_touched, o_lbuf, o_rbuf, o_skey, o_sval, o_pbuf, o_qbuf, o_arena;
   uint64_t arena_words;
   Desc* desc;          // [n_warps * MBE_MAXDEPTH]
   unsigned int* tops;  // [n_warps]
   unsigned int* stamps;  // [n_warps] persistent tag stamps
+  unsigned int* hint;    // [ceil(n_warps/32)] bit w set: warp w may hold a frame with unclaimed tasks
   Globals* gl;
   unsigned long long* per_root;  // device [nU*4] or NULL
   // bounded listing (device buffers) or cap_records = 0

@@ -40,14 +40,16 @@ struct __align__(16) WarpSmem {
   unsigned long long skey[MBE_SMEM_SORT];
   unsigned int sval[MBE_SMEM_SORT];
   unsigned int hist[256];
+  unsigned int foff[MBE_MAXDEPTH];  // arena word offset of the frame at each depth
+  unsigned int fnp[MBE_MAXDEPTH];   // its |P| (task count)
+  unsigned int pend[MBE_MAXDEPTH];  // prefetched claim result (PEND_NONE = none)
 };
+#define PEND_NONE 0xffffffffu
 
 struct Warp {
   int lane;
   uint32_t gw;
-  uint32_t* cnt;
-  uint32_t* bits;
-  unsigned long long* tag;
+  uint32_t* slot;  // [nU][8]: cnt, -, tag lo, tag hi, bits[4] (one 32-byte sector per vertex)
   uint32_t* touched;
   uint32_t* lbuf;
   uint32_t* rbuf;
@@ -63,9 +65,11 @@ struct Warp {
   uint32_t stamp;
   WarpSmem* sm;
   uint32_t cur_root;
+  bool failed;
   // lane-0 accumulators
   unsigned long long count, hash, tasks, pruned, steals, list_tasks, bitmap_tasks, frames, alg_bytes;
   uint32_t max_depth;
+  unsigned long long ph[8];  // MBE_STATS phase cycles (lane 0)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -490,6 +494,7 @@ __device__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lid
 __device__ __forceinline__ bool arena_reserve(Warp& w, const SearchParams& p, uint64_t words) {
   if (w.atop + words + 8 > w.arena_words || w.top + 1 >= MBE_MAXDEPTH) {
     if (w.lane == 0) set_error(p, w.top + 1 >= MBE_MAXDEPTH ? 2u : 1u, w.atop + words);
+    w.failed = true;
     return false;
   }
   return true;
@@ -502,9 +507,13 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
     Desc* d = &w.desc[w.top];
     d->off = (unsigned int)w.atop;
     d->done = 0u;
+    w.sm->foff[w.top] = (unsigned int)w.atop;
+    w.sm->fnp[w.top] = nP;
+    w.sm->pend[w.top] = PEND_NONE;
     __threadfence();
     atomicExch(&d->claim, ((unsigned long long)nP) << 32);
     p.tops[w.gw] = w.top + 1;
+    if (nP >= 2 && !(p.flags & F_NO_STEAL)) atomicOr(&p.hint[w.gw >> 5], 1u << (w.gw & 31));
     w.frames++;
   }
   w.atop = align4(w.atop + size_words);
@@ -557,6 +566,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     Lp = w.lbuf;
     if (nLp != key) {
       if (lane == 0) set_error(p, 3u, ((unsigned long long)nLp << 32) | key);
+      w.failed = true;
       return;
     }
   }
@@ -568,8 +578,10 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
   if (!root) {
     w.stamp++;
     const unsigned long long st = ((unsigned long long)w.stamp) << 32;
-    for (uint32_t j = lane; j < nP; j += 32) w.tag[Pid[j]] = st | (j + 1);
-    for (uint32_t j = lane; j < nR; j += 32) w.tag[R[j]] = st | TAG_R;
+    for (uint32_t j = lane; j < nP; j += 32)
+      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)Pid[j] * 8 + 2) = st | (j + 1);
+    for (uint32_t j = lane; j < nR; j += 32)
+      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)R[j] * 8 + 2) = st | TAG_R;
     __syncwarp();
   }
 
@@ -609,11 +621,11 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
       uint32_t v = 0;
       if (fv) {
         v = g.adjV[o_st + (f - (o_incl - o_d))];
-        uint32_t old = atomicAdd(&w.cnt[v], 1u);
+        uint32_t old = atomicAdd(&w.slot[(size_t)v * 8], 1u);
         isnew = (old == 0u);
         if (bm) {
           uint32_t pos = base + lo;
-          atomicOr(&w.bits[(size_t)v * Wc + (pos >> 5)], 1u << (pos & 31));
+          atomicOr(&w.slot[(size_t)v * 8 + 4 + (pos >> 5)], 1u << (pos & 31));
         }
       }
       uint32_t b = __ballot_sync(FULLMASK, isnew);
@@ -634,15 +646,18 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     uint32_t v = valid ? w.touched[t] : 0u;
     uint32_t c = 0;
     uint32_t rw[4] = {0u, 0u, 0u, 0u};
+    unsigned long long tg = 0;
     if (valid) {
-      c = w.cnt[v];
-      w.cnt[v] = 0u;
-      if (bm) {
-        for (uint32_t q = 0; q < Wc; ++q) {
-          rw[q] = w.bits[(size_t)v * Wc + q];
-          w.bits[(size_t)v * Wc + q] = 0u;
-        }
-      }
+      uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)v * 8);
+      uint4 a = sp[0], b = sp[1];
+      c = a.x;
+      tg = ((unsigned long long)a.w << 32) | a.z;
+      rw[0] = b.x;
+      rw[1] = b.y;
+      rw[2] = b.z;
+      rw[3] = b.w;
+      sp[0] = make_uint4(0u, 0u, 0u, 0u);
+      sp[1] = make_uint4(0u, 0u, 0u, 0u);
     }
     // role: 0 none/R, 1 Q-role, 2 P-role
     int role = 0;
@@ -650,7 +665,6 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
       if (root) {
         role = v == x ? 0 : (v < x ? 1 : 2);
       } else {
-        unsigned long long tg = w.tag[v];
         if ((uint32_t)(tg >> 32) == w.stamp) {
           uint32_t info = (uint32_t)tg;
           if (info == TAG_R) role = 0;
@@ -907,6 +921,10 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   publish_frame(w, p, size, nPc);
 }
 
+__device__ __forceinline__ int task_phase(const uint32_t* F) {
+  return (F[0] & 0xffu) == KIND_LIST ? 1 : 2;
+}
+
 __device__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
   const uint32_t h = F[0];
   w.cur_root = F[5];
@@ -918,6 +936,73 @@ __device__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint
     else if (W == 2) bitmap_task<2>(w, p, F, i);
     else bitmap_task<4>(w, p, F, i);
   }
+}
+
+__device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p) {
+  return (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+}
+
+// Idle warp: look for a published frame with unclaimed tasks in the warps
+// advertised by the hint bitmap, scanning circularly from gw+1,
+// and claim ONE task of the bottom-most such frame (largest subtree).
+// Returns true with (*victim, *depth, *task) on success.
+__device__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t* victim, uint32_t* depth,
+                          uint32_t* task) {
+  const int lane = w.lane;
+  const uint32_t nw = (p.n_warps + 31) >> 5;
+  const uint32_t start = ((w.gw + 1 + rot) % p.n_warps) >> 5;
+  int probes = 0;
+  for (uint32_t kb = 0; kb < nw && probes < 8; kb += 32) {
+    uint32_t k = kb + lane;
+    uint32_t word = k < nw ? ld_volatile(&p.hint[(start + k) % nw]) : 0u;
+    uint32_t have = __ballot_sync(FULLMASK, word != 0u);
+    while (have && probes < 8) {
+      int src = __ffs(have) - 1;
+      have &= have - 1;
+      uint32_t bitsv = __shfl_sync(FULLMASK, word, src);
+      uint32_t wi = (start + kb + src) % nw;
+      while (bitsv && probes < 8) {
+        int b = __ffs(bitsv) - 1;
+        bitsv &= bitsv - 1;
+        uint32_t v = wi * 32 + b;
+        if (v == w.gw || v >= p.n_warps) continue;
+        ++probes;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+          uint32_t tp = ld_volatile(&p.tops[v]);
+          const Desc* vd = p.desc + (size_t)v * MBE_MAXDEPTH;
+          int found = -1;
+          for (uint32_t db = 0; db < tp && found < 0; db += 32) {
+            uint32_t dd = db + lane;
+            bool ok = false;
+            if (dd < tp && dd < MBE_MAXDEPTH) {
+              unsigned long long c = ld_volatile64(&vd[dd].claim);
+              ok = (uint32_t)c < (uint32_t)(c >> 32);
+            }
+            uint32_t bb = __ballot_sync(FULLMASK, ok);
+            if (bb) found = (int)(db + __ffs(bb) - 1);
+          }
+          if (found >= 0) {
+            unsigned long long old = 0;
+            if (lane == 0) old = atomicAdd(&p.desc[(size_t)v * MBE_MAXDEPTH + found].claim, 1ull);
+            old = __shfl_sync(FULLMASK, old, 0);
+            if ((uint32_t)old < (uint32_t)(old >> 32)) {
+              *victim = v;
+              *depth = (uint32_t)found;
+              *task = (uint32_t)old;
+              return true;
+            }
+          }
+          if (attempt == 0) {
+            // nothing claimable: clear the hint bit, then re-check once (an owner that published
+            // after our scan set the bit before we cleared it, so its frame is visible now)
+            if (lane == 0) atomicAnd(&p.hint[v >> 5], ~(1u << (v & 31)));
+            __syncwarp();
+          }
+        }
+      }
+    }
+  }
+  return false;
 }
 
 // ================================================================== kernel
@@ -932,9 +1017,7 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
   w.lane = lane;
   w.gw = gw;
   uint8_t* base = p.ws + (size_t)gw * p.ws_stride;
-  w.cnt = reinterpret_cast<uint32_t*>(base + p.o_cnt);
-  w.bits = reinterpret_cast<uint32_t*>(base + p.o_bits);
-  w.tag = reinterpret_cast<unsigned long long*>(base + p.o_tag);
+  w.slot = reinterpret_cast<uint32_t*>(base + p.o_slot);
   w.touched = reinterpret_cast<uint32_t*>(base + p.o_touched);
   w.lbuf = reinterpret_cast<uint32_t*>(base + p.o_lbuf);
   w.rbuf = reinterpret_cast<uint32_t*>(base + p.o_rbuf);
@@ -950,45 +1033,69 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
   w.stamp = p.stamps[gw];
   w.sm = reinterpret_cast<WarpSmem*>(smem_raw) + wib;
   w.cur_root = 0;
+  w.failed = false;
   w.count = w.hash = w.tasks = w.pruned = w.steals = 0;
   w.list_tasks = w.bitmap_tasks = w.frames = w.alg_bytes = 0;
   w.max_depth = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w.ph[k] = 0;
 
   const bool steal = !(p.flags & F_NO_STEAL);
   bool roots_done = false;
   bool registered = false;
-  uint32_t backoff = 32;
+  uint32_t backoff = 64;
+  uint32_t rot = 0;
 
-  while (true) {
-    uint32_t err = 0;
-    if (lane == 0) err = ld_volatile(&p.gl->error);
-    if (__shfl_sync(FULLMASK, err, 0)) break;
+  while (!w.failed) {
     if (w.top > 0) {
-      Desc* d = &w.desc[w.top - 1];
-      unsigned long long old = 0;
-      if (lane == 0) old = atomicAdd(&d->claim, 1ull);
-      old = __shfl_sync(FULLMASK, old, 0);
-      const uint32_t nP = (uint32_t)(old >> 32), i = (uint32_t)old;
+      // ---- owner: next task of the top frame (claims go through the shared cursor so
+      // thieves can take siblings; the next claim is prefetched while this task runs)
+      const uint32_t d = w.top - 1;
+      Desc* dsc = &w.desc[d];
+      uint32_t i = 0;
+      if (lane == 0) {
+        i = w.sm->pend[d];
+        if (i == PEND_NONE) i = (uint32_t)atomicAdd(&dsc->claim, 1ull);
+      }
+      i = __shfl_sync(FULLMASK, i, 0);
+      const uint32_t nP = w.sm->fnp[d];
       if (i < nP) {
-        const uint32_t* F = w.arena + d->off;
+        unsigned long long nxt = PEND_NONE;
+        if (lane == 0) nxt = (i + 1 < nP) ? atomicAdd(&dsc->claim, 1ull) : (unsigned long long)nP;
+        const uint32_t* F = w.arena + w.sm->foff[d];
+        unsigned long long t0 = stats_clock(p);
         run_task(w, p, F, i);
         __syncwarp();
-        if (lane == 0) atomicAdd(&d->done, 1u);
-      } else {
         if (lane == 0) {
-          while (ld_volatile(&d->done) < nP && !ld_volatile(&p.gl->error)) __nanosleep(64);
-          atomicExch(&d->claim, 0ull);
-          d->done = 0u;
+          atomicAdd(&dsc->done, 1u);
+          w.sm->pend[d] = (uint32_t)nxt;
+          if (p.flags & F_STATS) w.ph[task_phase(F)] += clock64() - t0;
         }
-        const uint32_t off = d->off;
         __syncwarp();
-        w.top -= 1;
-        w.atop = off;
-        if (lane == 0) p.tops[gw] = w.top;
+      } else {
+        // exhausted: wait for thieves still reading it, then pop
+        unsigned long long t0 = stats_clock(p);
+        if (lane == 0) {
+          while (ld_volatile(&dsc->done) < nP) {
+            if (ld_volatile(&p.gl->error)) {
+              w.failed = true;
+              break;
+            }
+            __nanosleep(64);
+          }
+          atomicExch(&dsc->claim, 0ull);
+          dsc->done = 0u;
+          p.tops[gw] = d;
+          if (p.flags & F_STATS) w.ph[5] += clock64() - t0;
+        }
+        w.failed = __shfl_sync(FULLMASK, (int)w.failed, 0);
+        w.top = d;
+        w.atop = w.sm->foff[d];
+        __syncwarp();
       }
       continue;
     }
-    // empty stack: next level-1 subtree (coarse-grained task)
+    // ---- empty stack: next level-1 subtree (coarse-grained task)
     if (!roots_done) {
       unsigned long long pos = 0;
       if (lane == 0) {
@@ -999,12 +1106,15 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
       if (pos < p.g.n_roots) {
         const uint32_t x = p.g.root_order[pos];
         w.cur_root = x;
+        unsigned long long t0 = stats_clock(p);
         list_task(w, p, nullptr, 0u, x);
+        if (lane == 0 && (p.flags & F_STATS)) w.ph[0] += clock64() - t0;
         continue;
       }
       roots_done = true;
     }
-    // idle: register, then steal single tasks or terminate (SURVEY §7.2 termination)
+    // ---- idle: register, then steal single tasks or terminate
+    unsigned long long t0 = stats_clock(p);
     if (!registered) {
       if (lane == 0) atomicAdd(&p.gl->idle, 1u);
       registered = true;
@@ -1012,58 +1122,37 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
     uint32_t stop = 0;
     if (lane == 0) stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
     if (__shfl_sync(FULLMASK, stop, 0)) break;
-    if (!steal) {
-      __nanosleep(256);
-      continue;
+    uint32_t v = 0, dd = 0, ti = 0;
+    bool got = false;
+    if (steal) {
+      // leave the idle set while attempting, so termination cannot be declared under us
+      if (lane == 0) atomicSub(&p.gl->idle, 1u);
+      got = try_steal(w, p, rot, &v, &dd, &ti);
+      rot += 97;
+      if (!got && lane == 0) atomicAdd(&p.gl->idle, 1u);
     }
-    // scan victims circularly from gw+1 (as P:430-431); each lane probes one victim
-    int fv = -1, fd = -1;
-    for (uint32_t vb = 0; vb + 1 < p.n_warps && fv < 0; vb += 32) {
-      uint32_t t = vb + lane;
-      int myd = -1;
-      uint32_t v = (gw + 1 + t) % p.n_warps;
-      if (t + 1 < p.n_warps) {
-        uint32_t tp = ld_volatile(&p.tops[v]);
-        const Desc* vd = p.desc + (size_t)v * MBE_MAXDEPTH;
-        for (uint32_t dd = 0; dd < tp && dd < MBE_MAXDEPTH; ++dd) {
-          unsigned long long c = ld_volatile64(&vd[dd].claim);
-          if ((uint32_t)c < (uint32_t)(c >> 32)) {
-            myd = (int)dd;
-            break;
-          }
-        }
-      }
-      uint32_t b = __ballot_sync(FULLMASK, myd >= 0);
-      if (b) {
-        int src = __ffs(b) - 1;
-        fv = __shfl_sync(FULLMASK, (int)v, src);
-        fd = __shfl_sync(FULLMASK, myd, src);
-      }
-    }
-    if (fv < 0) {
+    if (!got) {
+      if (lane == 0 && (p.flags & F_STATS)) w.ph[3] += clock64() - t0;
+      unsigned long long t1 = stats_clock(p);
       __nanosleep(backoff);
-      if (backoff < 4096) backoff <<= 1;
+      if (backoff < 2048) backoff <<= 1;
+      if (lane == 0 && (p.flags & F_STATS)) w.ph[4] += clock64() - t1;
       continue;
     }
-    backoff = 32;
-    Desc* vd = p.desc + (size_t)fv * MBE_MAXDEPTH + fd;
-    unsigned long long old = 0;
-    if (lane == 0) {
-      atomicSub(&p.gl->idle, 1u);
-      old = atomicAdd(&vd->claim, 1ull);
-      if ((uint32_t)old >= (uint32_t)(old >> 32)) atomicAdd(&p.gl->idle, 1u);
-    }
-    old = __shfl_sync(FULLMASK, old, 0);
-    if ((uint32_t)old >= (uint32_t)(old >> 32)) continue;  // lost the race; still registered idle
+    backoff = 64;
     registered = false;
-    __threadfence();  // acquire: the victim published the frame before the claim word
+    __threadfence();  // acquire: the victim published the frame before its claim word
+    Desc* vd = p.desc + (size_t)v * MBE_MAXDEPTH + dd;
     const uint32_t off = ld_volatile(&vd->off);
-    const uint32_t* F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)fv * p.ws_stride + p.o_arena) + off;
-    run_task(w, p, F, (uint32_t)old);
+    const uint32_t* F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)v * p.ws_stride + p.o_arena) + off;
+    if (lane == 0 && (p.flags & F_STATS)) w.ph[3] += clock64() - t0;
+    unsigned long long t2 = stats_clock(p);
+    run_task(w, p, F, ti);
     __syncwarp();
     if (lane == 0) {
       w.steals++;
       atomicAdd(&vd->done, 1u);
+      if (p.flags & F_STATS) w.ph[task_phase(F)] += clock64() - t2;
     }
   }
 
@@ -1081,6 +1170,7 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
       atomicAdd(&p.gl->frames, w.frames);
       atomicAdd(&p.gl->alg_bytes, w.alg_bytes);
       atomicMax(&p.gl->max_depth, w.max_depth);
+      for (int k = 0; k < 8; ++k) atomicAdd(&p.gl->phase[k], w.ph[k]);
     }
   }
 }

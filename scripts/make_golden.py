@@ -1,0 +1,54 @@
+"""Write tests/golden/configs.txt: oracle (count, hash, tasks, pruned) of the
+full-size configs.  Calls ONLY oracle/ (and the shared input generator).
+
+    python scripts/make_golden.py C2 C3 [--threads N]
+
+Existing rows for other configs are kept.  Each row records the oracle's wall
+time and thread count on the machine that produced it.
+"""
+import argparse
+import os
+import platform
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_2401_05039_b200 import inputs as I  # noqa: E402
+
+PATH = os.path.join(ROOT, "tests", "golden", "configs.txt")
+HEADER = """# Oracle results on the full-size synthetic configs (SURVEY.md §8(d), BASELINE.json configs[1..4]).
+# Written by scripts/make_golden.py, which calls only oracle/ (plain Algorithm 1, P:118-169) on the
+# graphs of paper_2401_05039_b200/inputs.py.  Columns: config count hash tasks pruned oracle_seconds threads host
+"""
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--out", default=PATH)
+    a = ap.parse_args()
+    out = a.out
+    rows = {}
+    if os.path.exists(out):
+        for line in open(out):
+            if line.strip() and not line.startswith("#"):
+                rows[line.split()[0]] = line.rstrip("\n")
+    for c in a.configs:
+        g = I.config_graph(c)
+        t = time.time()
+        r = oracle.mbea(g, threads=a.threads)
+        dt = time.time() - t
+        rows[c] = f"{c} {r.count} {r.hash:#018x} {r.tasks} {r.pruned} {dt:.1f} {r.threads} {platform.node()}"
+        print(rows[c], flush=True)
+        with open(out, "w") as f:
+            f.write(HEADER)
+            for k in sorted(rows):
+                f.write(rows[k] + "\n")
+
+
+if __name__ == "__main__":
+    main()
