@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -423,6 +424,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.world = cfg.world;
     p.claim_counter = reinterpret_cast<unsigned long long*>(cfg.claim_counter);
     p.n_warps = n_warps;
+    {
+      const char* wd = std::getenv("MBE_WATCHDOG_MS");
+      p.watchdog_ns = (wd ? std::strtoull(wd, nullptr, 10) : 120000ull) * 1000000ull;
+    }
     p.ws = static_cast<uint8_t*>(g->ws.p);
     p.ws_stride = g->ws_stride;
     p.arena_words = arena / 4;
@@ -462,7 +467,9 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
         arena *= 4;  // auto arena: grow and retry
         continue;
       }
-      if (hg.error == 3u) {
+      if (hg.error == 4u) {
+        result = fail(MBE_EINTERNAL, "device watchdog expired (MBE_WATCHDOG_MS)");
+      } else if (hg.error == 3u) {
         result = fail(MBE_EINTERNAL, "device consistency check failed (info " + std::to_string(hg.err_info) + ")");
       } else {
         result = fail(MBE_EOVERFLOW, hg.error == 2u ? "stack depth > " + std::to_string(MBE_MAXDEPTH)

@@ -36,7 +36,7 @@ struct Desc {
 struct Globals {
   unsigned long long root_cursor;
   unsigned int idle;
-  unsigned int error;  // 0 ok, 1 arena overflow, 2 depth overflow, 3 internal check
+  unsigned int error;  // 0 ok, 1 arena overflow, 2 depth overflow, 3 internal check, 4 watchdog
   unsigned long long count, hash, tasks, pruned, steals;
   unsigned long long list_tasks, bitmap_tasks, frames, alg_bytes;
   unsigned int max_depth;
@@ -54,6 +54,7 @@ struct SearchParams {
   uint32_t rank, world;
   unsigned long long* claim_counter;  // NULL -> static deal
   uint32_t n_warps;
+  unsigned long long watchdog_ns;  // abort (error 4) if a warp idles/waits past this since launch
   // per-warp workspace: region w starts at ws + w * ws_stride (bytes); offsets below are bytes
   uint8_t* ws;
   uint64_t ws_stride;

@@ -89,6 +89,12 @@ __device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long 
   return *(volatile const unsigned long long*)p;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void set_error(const SearchParams& p, unsigned int code, unsigned long long info) {
   if (atomicCAS(&p.gl->error, 0u, code) == 0u) p.gl->err_info = info;
 }
@@ -982,8 +988,14 @@ __device__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t
             if (bb) found = (int)(db + __ffs(bb) - 1);
           }
           if (found >= 0) {
+            // leave the idle set before claiming, so termination cannot be declared while this
+            // warp holds a claimed task; re-enter it if the claim is lost
             unsigned long long old = 0;
-            if (lane == 0) old = atomicAdd(&p.desc[(size_t)v * MBE_MAXDEPTH + found].claim, 1ull);
+            if (lane == 0) {
+              atomicSub(&p.gl->idle, 1u);
+              old = atomicAdd(&p.desc[(size_t)v * MBE_MAXDEPTH + found].claim, 1ull);
+              if ((uint32_t)old >= (uint32_t)(old >> 32)) atomicAdd(&p.gl->idle, 1u);
+            }
             old = __shfl_sync(FULLMASK, old, 0);
             if ((uint32_t)old < (uint32_t)(old >> 32)) {
               *victim = v;
@@ -1041,6 +1053,7 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
   for (int k = 0; k < 8; ++k) w.ph[k] = 0;
 
   const bool steal = !(p.flags & F_NO_STEAL);
+  const unsigned long long t_start = globaltimer_ns();
   bool roots_done = false;
   bool registered = false;
   uint32_t backoff = 64;
@@ -1077,7 +1090,8 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
         unsigned long long t0 = stats_clock(p);
         if (lane == 0) {
           while (ld_volatile(&dsc->done) < nP) {
-            if (ld_volatile(&p.gl->error)) {
+            if (ld_volatile(&p.gl->error) || globaltimer_ns() - t_start > p.watchdog_ns) {
+              set_error(p, 4u, 1ull);
               w.failed = true;
               break;
             }
@@ -1120,16 +1134,19 @@ __global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
       registered = true;
     }
     uint32_t stop = 0;
-    if (lane == 0) stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
+    if (lane == 0) {
+      stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
+      if (!stop && globaltimer_ns() - t_start > p.watchdog_ns) {
+        set_error(p, 4u, 0ull);  // watchdog: never hang the device
+        stop = 1;
+      }
+    }
     if (__shfl_sync(FULLMASK, stop, 0)) break;
     uint32_t v = 0, dd = 0, ti = 0;
     bool got = false;
     if (steal) {
-      // leave the idle set while attempting, so termination cannot be declared under us
-      if (lane == 0) atomicSub(&p.gl->idle, 1u);
-      got = try_steal(w, p, rot, &v, &dd, &ti);
+      got = try_steal(w, p, rot, &v, &dd, &ti);  // leaves the idle set only on a successful claim
       rot += 97;
-      if (!got && lane == 0) atomicAdd(&p.gl->idle, 1u);
     }
     if (!got) {
       if (lane == 0 && (p.flags & F_STATS)) w.ph[3] += clock64() - t0;
