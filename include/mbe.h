@@ -128,10 +128,14 @@ typedef struct {
   uint64_t n_edges;       /* after deduplication */
   uint32_t max_deg1, max_deg2;
   int32_t device;
+  uint64_t h2d_bytes;     /* bytes copied host -> device by ingest so far */
 } mbe_graph_info;
 int mbe_get_info(const mbe_graph *g, mbe_graph_info *info);
 
-void mbe_free(mbe_graph *g);             /* NULL-safe; releases host and device memory */
+void mbe_free(mbe_graph *g);             /* NULL-safe; releases the graph's host and device memory */
+/* Search workspaces (per-warp scratch + frame arenas) are pooled per device and
+ * reused across handles; this frees every pooled workspace not in use. */
+void mbe_release_workspaces(void);
 const char *mbe_strerror(int code);      /* static string */
 const char *mbe_last_error_detail(void); /* thread-local message of the last failing call */
 

@@ -23,5 +23,6 @@ from ._lib import (  # noqa: F401
     mbe_get_info,
     mbe_last_error_detail,
     mbe_load_csr,
+    mbe_release_workspaces,
     mbe_strerror,
 )

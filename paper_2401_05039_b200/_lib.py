@@ -21,8 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libmbe.so")
 MBE_OK, MBE_EINVAL, MBE_ENOMEM, MBE_ECUDA, MBE_EOVERFLOW, MBE_ERANGE, MBE_EDIST, MBE_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7
 MBE_NO_STEAL, MBE_STATS, MBE_NO_ANTICHAIN, MBE_NO_TWIN = 0x1, 0x2, 0x4, 0x8
 
-EXPORTED_SYMBOLS = ("mbe_load_csr", "mbe_enumerate", "mbe_get_info", "mbe_free", "mbe_strerror",
-                    "mbe_last_error_detail")
+EXPORTED_SYMBOLS = ("mbe_load_csr", "mbe_enumerate", "mbe_get_info", "mbe_free", "mbe_release_workspaces",
+                    "mbe_strerror", "mbe_last_error_detail")
 
 _u32, _i32, _u64, _dbl, _vp = ctypes.c_uint32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 _p64, _p32 = ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)
@@ -49,7 +49,7 @@ class mbe_result(ctypes.Structure):
 
 class mbe_graph_info(ctypes.Structure):
     _fields_ = [("n1", _u32), ("n2", _u32), ("n_edges", _u64), ("max_deg1", _u32), ("max_deg2", _u32),
-                ("device", _i32)]
+                ("device", _i32), ("h2d_bytes", _u64)]
 
 
 _lock = threading.Lock()
@@ -84,6 +84,8 @@ def load_library():
             lib.mbe_get_info.restype = ctypes.c_int
             lib.mbe_free.argtypes = [_vp]
             lib.mbe_free.restype = None
+            lib.mbe_release_workspaces.argtypes = []
+            lib.mbe_release_workspaces.restype = None
             lib.mbe_strerror.argtypes = [ctypes.c_int]
             lib.mbe_strerror.restype = ctypes.c_char_p
             lib.mbe_last_error_detail.argtypes = []
@@ -180,6 +182,10 @@ def mbe_get_info(handle: int) -> dict:
 def mbe_free(handle: int) -> None:
     if handle:
         load_library().mbe_free(ctypes.c_void_p(handle))
+
+
+def mbe_release_workspaces() -> None:
+    load_library().mbe_release_workspaces()
 
 
 class MBEGraph:

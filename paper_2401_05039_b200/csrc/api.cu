@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -48,11 +49,14 @@ struct DevBuf {
   }
 };
 
+thread_local uint64_t* g_upload_counter = nullptr;
+
 template <class T>
 int upload(DevBuf& b, const std::vector<T>& v) {
   size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
   if (cudaMalloc(&b.p, bytes) != cudaSuccess) return fail(MBE_ENOMEM, "cudaMalloc graph");
   b.bytes = bytes;
+  if (g_upload_counter) *g_upload_counter += v.size() * sizeof(T);
   if (!v.empty()) CUDA_TRY(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   return MBE_OK;
 }
@@ -69,6 +73,25 @@ struct Side {
   }
 };
 
+// Search workspace (per-warp scratch + frame arenas + descriptors).  Pooled
+// process-wide per device and checked out exclusively by one mbe_enumerate
+// call at a time, so load -> enumerate -> free cycles do not re-allocate GBs.
+struct Workspace {
+  int device = 0;
+  bool busy = false, dirty = true;
+  uint32_t n_warps = 0, wmax = 0;
+  uint64_t cap_nU = 0, cap_lbuf = 0, arena_bytes = 0, stride = 0;
+  uint64_t o_slot = 0, o_touched = 0, o_lbuf = 0, o_rbuf = 0, o_skey = 0, o_sval = 0, o_pbuf = 0, o_qbuf = 0,
+           o_arena = 0;
+  DevBuf ws, desc, tops, stamps, hint, per_root, gl;
+  void release() {
+    for (DevBuf* b : {&ws, &desc, &tops, &stamps, &hint, &per_root, &gl}) b->release();
+  }
+};
+
+std::mutex g_pool_mu;
+std::vector<Workspace*> g_pool;
+
 }  // namespace
 
 struct mbe_graph {
@@ -78,17 +101,12 @@ struct mbe_graph {
   // deduplicated host CSR in both directions (original ids)
   std::vector<uint32_t> off1, adj1, off2, adj2;
   Side side[2];
-  // workspace cache
-  DevBuf ws, desc, tops, stamps, hint, gl, per_root;
-  uint64_t ws_stride = 0, arena_bytes = 0;
-  uint32_t ws_warps = 0, ws_side = 0, ws_wmax = 0;
-  bool ws_dirty = true;
+  uint64_t h2d_bytes = 0;  // bytes uploaded by ingest (all built sides)
   SearchParams sp;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int sm_count = 0;
   ~mbe_graph() {
     for (auto& s : side) s.release();
-    for (DevBuf* b : {&ws, &desc, &tops, &stamps, &hint, &gl, &per_root}) b->release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
   }
@@ -100,6 +118,7 @@ namespace {
 int build_side(mbe_graph* g, int s) {
   Side& S = g->side[s - 1];
   if (S.built) return MBE_OK;
+  g_upload_counter = &g->h2d_bytes;
   const std::vector<uint32_t>& offC = s == 1 ? g->off1 : g->off2;  // candidate side CSR
   const std::vector<uint32_t>& adjC = s == 1 ? g->adj1 : g->adj2;
   const uint32_t nU = s == 1 ? g->n1 : g->n2, nV = s == 1 ? g->n2 : g->n1;
@@ -177,57 +196,93 @@ int build_side(mbe_graph* g, int s) {
 
 uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
-int ensure_workspace(mbe_graph* g, int s, uint32_t n_warps, uint64_t arena_bytes, uint32_t wmax) {
-  Side& S = g->side[s - 1];
-  if (g->ws.p && g->ws_warps == n_warps && g->ws_side == (uint32_t)s && g->arena_bytes == arena_bytes &&
-      g->ws_wmax == wmax) {
-    return MBE_OK;
+// Check out a workspace able to run n_warps warps over nU candidate vertices.
+int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t maxdeg, uint64_t arena_bytes,
+                       uint32_t wmax, Workspace** out) {
+  nU = std::max<uint64_t>(nU, 1);
+  const uint64_t lb = std::max<uint64_t>(maxdeg, 32 * MBE_WMAX);
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (Workspace* w : g_pool)
+      if (!w->busy && w->device == device && w->n_warps == n_warps && w->cap_nU >= nU && w->cap_lbuf >= lb &&
+          w->arena_bytes == arena_bytes && w->wmax >= wmax) {
+        w->busy = true;
+        *out = w;
+        return MBE_OK;
+      }
   }
-  for (DevBuf* b : {&g->ws, &g->desc, &g->tops, &g->stamps, &g->hint, &g->per_root}) b->release();
-  const uint64_t nU = std::max<uint32_t>(S.nU, 1);
-  SearchParams& p = g->sp;
+  Workspace* w = new Workspace();
+  w->device = device;
+  w->n_warps = n_warps;
+  w->wmax = wmax;
+  w->cap_nU = nU;
+  w->cap_lbuf = lb;
+  w->arena_bytes = arena_bytes;
   uint64_t o = 0;
-  p.o_slot = o; o = align256(o + nU * 32);
-  p.o_touched = o; o = align256(o + nU * 4);
-  p.o_lbuf = o; o = align256(o + (uint64_t)std::max<uint32_t>(S.maxdegU, 32 * MBE_WMAX) * 4);
-  p.o_rbuf = o; o = align256(o + nU * 4);
-  p.o_skey = o; o = align256(o + nU * 16);
-  p.o_sval = o; o = align256(o + nU * 8);
-  p.o_pbuf = o; o = align256(o + nU * wmax * 4);
-  p.o_qbuf = o; o = align256(o + nU * wmax * 4);
-  p.o_arena = o; o = align256(o + arena_bytes);
-  g->ws_stride = o;
+  w->o_slot = o; o = align256(o + nU * 32);
+  w->o_touched = o; o = align256(o + nU * 4);
+  w->o_lbuf = o; o = align256(o + lb * 4);
+  w->o_rbuf = o; o = align256(o + nU * 4);
+  w->o_skey = o; o = align256(o + nU * 16);
+  w->o_sval = o; o = align256(o + nU * 8);
+  w->o_pbuf = o; o = align256(o + nU * wmax * 4);
+  w->o_qbuf = o; o = align256(o + nU * wmax * 4);
+  w->o_arena = o; o = align256(o + arena_bytes);
+  w->stride = o;
   const uint64_t total = o * n_warps;
-  if (cudaMalloc(&g->ws.p, total) != cudaSuccess) {
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (cudaMalloc(&w->ws.p, total) == cudaSuccess) break;
     cudaGetLastError();
+    w->ws.p = nullptr;
+    if (attempt == 0) {  // free idle pooled workspaces of this device and retry once
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      for (auto it = g_pool.begin(); it != g_pool.end();) {
+        if (!(*it)->busy && (*it)->device == device) {
+          (*it)->release();
+          delete *it;
+          it = g_pool.erase(it);
+        } else {
+          ++it;
+        }
+      }
+    }
+  }
+  if (!w->ws.p) {
+    delete w;
     return fail(MBE_ENOMEM, "workspace of " + std::to_string(total >> 20) + " MiB (" + std::to_string(n_warps) +
                                 " warps): reduce ctas_per_sm/threads_per_cta/arena_bytes");
   }
-  g->ws.bytes = total;
-  if (cudaMalloc(&g->desc.p, sizeof(Desc) * MBE_MAXDEPTH * n_warps) != cudaSuccess ||
-      cudaMalloc(&g->tops.p, 4ull * n_warps) != cudaSuccess || cudaMalloc(&g->stamps.p, 4ull * n_warps) != cudaSuccess ||
-      cudaMalloc(&g->hint.p, 4ull * ((n_warps + 31) / 32)) != cudaSuccess ||
-      cudaMalloc(&g->per_root.p, 32ull * nU) != cudaSuccess) {
+  w->ws.bytes = total;
+  if (cudaMalloc(&w->desc.p, sizeof(Desc) * MBE_MAXDEPTH * n_warps) != cudaSuccess ||
+      cudaMalloc(&w->tops.p, 4ull * n_warps) != cudaSuccess || cudaMalloc(&w->stamps.p, 4ull * n_warps) != cudaSuccess ||
+      cudaMalloc(&w->hint.p, 4ull * ((n_warps + 31) / 32)) != cudaSuccess ||
+      cudaMalloc(&w->per_root.p, 32ull * nU) != cudaSuccess || cudaMalloc(&w->gl.p, sizeof(Globals)) != cudaSuccess) {
     cudaGetLastError();
+    w->release();
+    delete w;
     return fail(MBE_ENOMEM, "workspace descriptors");
   }
-  CUDA_TRY(cudaMemset(g->stamps.p, 0, 4ull * n_warps));
-  g->ws_warps = n_warps;
-  g->ws_side = s;
-  g->arena_bytes = arena_bytes;
-  g->ws_wmax = wmax;
-  g->ws_dirty = true;  // counters/bits/tags must be zeroed before use
+  w->busy = true;
+  w->dirty = true;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(w);
+  }
+  *out = w;
   return MBE_OK;
 }
 
-// zero the per-warp cnt/bits/tag tables (required invariant: zero between tasks)
-int clear_tables(mbe_graph* g, cudaStream_t st) {
-  const SearchParams& p = g->sp;
-  // per-vertex slots (count, tag, bit row) must be zero between tasks
-  CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(g->ws.p) + p.o_slot, g->ws_stride, 0, p.o_touched - p.o_slot,
-                             g->ws_warps, st));
-  CUDA_TRY(cudaMemsetAsync(g->stamps.p, 0, 4ull * g->ws_warps, st));
-  g->ws_dirty = false;
+void checkin_workspace(Workspace* w) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  w->busy = false;
+}
+
+// zero the per-vertex slots (required invariant: zero between tasks) and the tag stamps
+int clear_tables(Workspace* w, cudaStream_t st) {
+  CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(w->ws.p) + w->o_slot, w->stride, 0, w->o_touched - w->o_slot,
+                             w->n_warps, st));
+  CUDA_TRY(cudaMemsetAsync(w->stamps.p, 0, 4ull * w->n_warps, st));
+  w->dirty = false;
   return MBE_OK;
 }
 
@@ -333,6 +388,7 @@ int mbe_get_info(const mbe_graph* g, mbe_graph_info* info) {
   info->max_deg1 = m1;
   info->max_deg2 = m2;
   info->device = g->device;
+  info->h2d_bytes = g->h2d_bytes;
   return MBE_OK;
 }
 
@@ -385,23 +441,39 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cfg.stream);
 
   // listing buffers (device) for this call
-  DevBuf d_rec_off, d_n1, d_n2, d_ids;
+  struct BufGuard {
+    DevBuf rec_off, n1, n2, ids;
+    ~BufGuard() {
+      for (DevBuf* b : {&rec_off, &n1, &n2, &ids}) b->release();
+    }
+  } lb;
   const uint64_t cap_rec = out ? out->cap_records : 0, cap_ids = out ? out->cap_ids : 0;
   if (cap_rec) {
-    if (cudaMalloc(&d_rec_off.p, 8 * cap_rec) != cudaSuccess || cudaMalloc(&d_n1.p, 4 * cap_rec) != cudaSuccess ||
-        cudaMalloc(&d_n2.p, 4 * cap_rec) != cudaSuccess || cudaMalloc(&d_ids.p, 4 * std::max<uint64_t>(cap_ids, 1)) != cudaSuccess) {
+    if (cudaMalloc(&lb.rec_off.p, 8 * cap_rec) != cudaSuccess || cudaMalloc(&lb.n1.p, 4 * cap_rec) != cudaSuccess ||
+        cudaMalloc(&lb.n2.p, 4 * cap_rec) != cudaSuccess ||
+        cudaMalloc(&lb.ids.p, 4 * std::max<uint64_t>(cap_ids, 1)) != cudaSuccess) {
       cudaGetLastError();
-      for (DevBuf* b : {&d_rec_off, &d_n1, &d_n2, &d_ids}) b->release();
       return fail(MBE_ENOMEM, "listing buffers");
     }
   }
-  if (!g->gl.p && cudaMalloc(&g->gl.p, sizeof(Globals)) != cudaSuccess) return fail(MBE_ENOMEM, "globals");
+  struct WsGuard {
+    Workspace* w = nullptr;
+    ~WsGuard() {
+      if (w) checkin_workspace(w);
+    }
+  } wg;
 
-  int result = MBE_OK;
   for (int attempt = 0;; ++attempt) {
-    rc = ensure_workspace(g, side, n_warps, arena, wmax);
-    if (rc) { result = rc; break; }
-    if (g->ws_dirty && (rc = clear_tables(g, st))) { result = rc; break; }
+    if (wg.w && wg.w->arena_bytes != arena) {
+      checkin_workspace(wg.w);
+      wg.w = nullptr;
+    }
+    if (!wg.w) {
+      rc = checkout_workspace(g->device, n_warps, S.nU, S.maxdegU, arena, wmax, &wg.w);
+      if (rc) return rc;
+    }
+    Workspace* W = wg.w;
+    if (W->dirty && (rc = clear_tables(W, st))) return rc;
     SearchParams& p = g->sp;
     p.g.nU = S.nU;
     p.g.nV = S.nV;
@@ -428,54 +500,56 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       const char* wd = std::getenv("MBE_WATCHDOG_MS");
       p.watchdog_ns = (wd ? std::strtoull(wd, nullptr, 10) : 120000ull) * 1000000ull;
     }
-    p.ws = static_cast<uint8_t*>(g->ws.p);
-    p.ws_stride = g->ws_stride;
+    p.ws = static_cast<uint8_t*>(W->ws.p);
+    p.ws_stride = W->stride;
+    p.o_slot = W->o_slot;
+    p.o_touched = W->o_touched;
+    p.o_lbuf = W->o_lbuf;
+    p.o_rbuf = W->o_rbuf;
+    p.o_skey = W->o_skey;
+    p.o_sval = W->o_sval;
+    p.o_pbuf = W->o_pbuf;
+    p.o_qbuf = W->o_qbuf;
+    p.o_arena = W->o_arena;
+    p.skey2_off = W->cap_nU;
     p.arena_words = arena / 4;
-    p.desc = static_cast<Desc*>(g->desc.p);
-    p.tops = static_cast<unsigned int*>(g->tops.p);
-    p.stamps = static_cast<unsigned int*>(g->stamps.p);
-    p.hint = static_cast<unsigned int*>(g->hint.p);
-    p.gl = static_cast<Globals*>(g->gl.p);
-    p.per_root = cfg.per_root ? static_cast<unsigned long long*>(g->per_root.p) : nullptr;
+    p.desc = static_cast<Desc*>(W->desc.p);
+    p.tops = static_cast<unsigned int*>(W->tops.p);
+    p.stamps = static_cast<unsigned int*>(W->stamps.p);
+    p.hint = static_cast<unsigned int*>(W->hint.p);
+    p.gl = static_cast<Globals*>(W->gl.p);
+    p.per_root = cfg.per_root ? static_cast<unsigned long long*>(W->per_root.p) : nullptr;
     p.cap_records = cap_rec;
     p.cap_ids = cap_ids;
-    p.rec_off = (unsigned long long*)d_rec_off.p;
-    p.rec_n1 = (unsigned int*)d_n1.p;
-    p.rec_n2 = (unsigned int*)d_n2.p;
-    p.out_ids = (unsigned int*)d_ids.p;
+    p.rec_off = (unsigned long long*)lb.rec_off.p;
+    p.rec_n1 = (unsigned int*)lb.n1.p;
+    p.rec_n2 = (unsigned int*)lb.n2.p;
+    p.out_ids = (unsigned int*)lb.ids.p;
 
-    CUDA_TRY(cudaMemsetAsync(g->gl.p, 0, sizeof(Globals), st));
-    CUDA_TRY(cudaMemsetAsync(g->desc.p, 0, sizeof(Desc) * MBE_MAXDEPTH * n_warps, st));
-    CUDA_TRY(cudaMemsetAsync(g->tops.p, 0, 4ull * n_warps, st));
-    CUDA_TRY(cudaMemsetAsync(g->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
-    if (p.per_root) CUDA_TRY(cudaMemsetAsync(g->per_root.p, 0, 32ull * S.nU, st));
+    CUDA_TRY(cudaMemsetAsync(W->gl.p, 0, sizeof(Globals), st));
+    CUDA_TRY(cudaMemsetAsync(W->desc.p, 0, sizeof(Desc) * MBE_MAXDEPTH * n_warps, st));
+    CUDA_TRY(cudaMemsetAsync(W->tops.p, 0, 4ull * n_warps, st));
+    CUDA_TRY(cudaMemsetAsync(W->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
+    if (p.per_root) CUDA_TRY(cudaMemsetAsync(W->per_root.p, 0, 32ull * S.nU, st));
     const int smem = mbe_search_smem_per_warp() * (int)(threads / 32);
-    CUDA_TRY(cudaEventRecord(g->ev0, st));
-    if (mbe_launch_search(p, (int)grid, (int)threads, smem, st) != 0) {
-      result = fail(MBE_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(cudaGetLastError()));
-      break;
-    }
-    CUDA_TRY(cudaEventRecord(g->ev1, st));
+    if (mbe_launch_search(p, (int)grid, (int)threads, smem, st, g->ev0, g->ev1) != 0)
+      return fail(MBE_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(cudaGetLastError()));
     Globals hg;
-    CUDA_TRY(cudaMemcpyAsync(&hg, g->gl.p, sizeof(Globals), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&hg, W->gl.p, sizeof(Globals), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
     if (hg.error) {
-      g->ws_dirty = true;  // tables may hold partial counts
+      W->dirty = true;  // slots may hold partial counts
       if ((hg.error == 1u) && !cfg.arena_bytes && attempt < 6) {
         arena *= 4;  // auto arena: grow and retry
         continue;
       }
-      if (hg.error == 4u) {
-        result = fail(MBE_EINTERNAL, "device watchdog expired (MBE_WATCHDOG_MS)");
-      } else if (hg.error == 3u) {
-        result = fail(MBE_EINTERNAL, "device consistency check failed (info " + std::to_string(hg.err_info) + ")");
-      } else {
-        result = fail(MBE_EOVERFLOW, hg.error == 2u ? "stack depth > " + std::to_string(MBE_MAXDEPTH)
-                                                    : "frame arena exhausted (arena_bytes=" + std::to_string(arena) + ")");
-      }
-      break;
+      if (hg.error == 4u) return fail(MBE_EINTERNAL, "device watchdog expired (MBE_WATCHDOG_MS)");
+      if (hg.error == 3u)
+        return fail(MBE_EINTERNAL, "device consistency check failed (info " + std::to_string(hg.err_info) + ")");
+      return fail(MBE_EOVERFLOW, hg.error == 2u ? "stack depth > " + std::to_string(MBE_MAXDEPTH)
+                                                : "frame arena exhausted (arena_bytes=" + std::to_string(arena) + ")");
     }
     res->count = hg.count;
     res->hash = hg.hash;
@@ -492,18 +566,17 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     for (int k = 0; k < 8; ++k) res->phase_cycles[k] = hg.phase[k];
     if (cfg.per_root) {
       std::vector<uint64_t> pr(4ull * S.nU);
-      CUDA_TRY(cudaMemcpy(pr.data(), g->per_root.p, 32ull * S.nU, cudaMemcpyDeviceToHost));
-      for (uint32_t r = 0; r < S.nU; ++r)
-        std::memcpy(cfg.per_root + 4ull * S.origU[r], pr.data() + 4ull * r, 32);
+      CUDA_TRY(cudaMemcpy(pr.data(), W->per_root.p, 32ull * S.nU, cudaMemcpyDeviceToHost));
+      for (uint32_t r = 0; r < S.nU; ++r) std::memcpy(cfg.per_root + 4ull * S.origU[r], pr.data() + 4ull * r, 32);
     }
     if (cap_rec) {
       uint64_t nrec = std::min<uint64_t>(hg.out_records, cap_rec);
       std::vector<uint64_t> ro(nrec);
       std::vector<uint32_t> a(nrec), b(nrec);
       if (nrec) {
-        CUDA_TRY(cudaMemcpy(ro.data(), d_rec_off.p, 8 * nrec, cudaMemcpyDeviceToHost));
-        CUDA_TRY(cudaMemcpy(a.data(), d_n1.p, 4 * nrec, cudaMemcpyDeviceToHost));
-        CUDA_TRY(cudaMemcpy(b.data(), d_n2.p, 4 * nrec, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(ro.data(), lb.rec_off.p, 8 * nrec, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(a.data(), lb.n1.p, 4 * nrec, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(b.data(), lb.n2.p, 4 * nrec, cudaMemcpyDeviceToHost));
       }
       // keep only records whose ids fit entirely
       uint64_t written = 0;
@@ -515,7 +588,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
         ++written;
       }
       uint64_t nid = std::min<uint64_t>(hg.out_ids, cap_ids);
-      if (nid) CUDA_TRY(cudaMemcpy(out->ids, d_ids.p, 4 * nid, cudaMemcpyDeviceToHost));
+      if (nid) CUDA_TRY(cudaMemcpy(out->ids, lb.ids.p, 4 * nid, cudaMemcpyDeviceToHost));
       for (uint64_t r = 0; r < written; ++r) {  // canonical order inside each side
         std::sort(out->ids + out->rec_off[r], out->ids + out->rec_off[r] + out->rec_n1[r]);
         std::sort(out->ids + out->rec_off[r] + out->rec_n1[r],
@@ -526,9 +599,25 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     }
     break;
   }
-  for (DevBuf* b : {&d_rec_off, &d_n1, &d_n2, &d_ids}) b->release();
   res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  return result;
+  return MBE_OK;
+}
+
+void mbe_release_workspaces(void) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (auto it = g_pool.begin(); it != g_pool.end();) {
+    if (!(*it)->busy) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaSetDevice((*it)->device);
+      (*it)->release();
+      cudaSetDevice(dev);
+      delete *it;
+      it = g_pool.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
 }  // extern "C"

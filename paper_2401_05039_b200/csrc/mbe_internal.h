@@ -59,6 +59,7 @@ struct SearchParams {
   uint8_t* ws;
   uint64_t ws_stride;
   uint64_t o_slot, o_touched, o_lbuf, o_rbuf, o_skey, o_sval, o_pbuf, o_qbuf, o_arena;
+  uint64_t skey2_off;  // element offset of the second (ping-pong) sort buffers
   uint64_t arena_words;
   Desc* desc;          // [n_warps * MBE_MAXDEPTH]
   unsigned int* tops;  // [n_warps]
@@ -80,5 +81,7 @@ struct SearchParams {
 #define F_NO_ANTICHAIN 0x4u
 #define F_NO_TWIN 0x8u
 
-int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream);
+// Launches the twin pre-pass and the persistent search kernel on `stream`;
+// ev0/ev1 (cudaEvent_t) bracket the search kernel alone.
+int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1);
 int mbe_search_smem_per_warp();

@@ -327,8 +327,8 @@ __device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint
     sort_smem(w.skey, w.sval, n, w.sm, w.lane);
   } else {
     // second buffers live right after the first ones (same per-warp region, sized nU)
-    unsigned long long* key2 = w.skey + p.g.nU;
-    uint32_t* val2 = w.sval + p.g.nU;
+    unsigned long long* key2 = w.skey + p.skey2_off;
+    uint32_t* val2 = w.sval + p.skey2_off;
     sort_radix(w.skey, w.sval, key2, val2, n, bit_length(p.g.nU), bit_length(max_count), w.sm, w.lane);
   }
 }
@@ -1256,7 +1256,7 @@ __global__ void __launch_bounds__(256) mbe_twin_kernel(DevGraph g, uint8_t* twin
 
 int mbe_search_smem_per_warp() { return (int)sizeof(WarpSmem); }
 
-int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream) {
+int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!(p.flags & F_NO_TWIN)) {
     mbe_twin_kernel<<<148 * 8, 256, 0, s>>>(p.g, const_cast<uint8_t*>(p.g.twin));
@@ -1269,6 +1269,8 @@ int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes
       return -1;
     attr_set = true;
   }
+  if (cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev0), s) != cudaSuccess) return -1;
   mbe_search_kernel<<<grid, block, smem_bytes, s>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+  if (cudaGetLastError() != cudaSuccess) return -1;
+  return cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev1), s) == cudaSuccess ? 0 : -1;
 }
