@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
     if not force and up_to_date():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2",
+    defs = [f"-D{d}" for d in os.environ.get("MBE_DEFINES", "").split() if d]
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O2", *defs,
            "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), *extra]
     if verbose:
         cmd += ["-Xptxas", "-v"]

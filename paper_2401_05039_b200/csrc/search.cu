@@ -611,32 +611,41 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     }
     const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
     visits += total;
-    for (uint32_t fb = 0; fb < total; fb += 32) {
-      uint32_t f = fb + lane;
-      bool fv = f < total;
-      int lo = 0;
+    // 4 flattened visits per lane per iteration: independent loads/atomics in flight (MLP)
+    for (uint32_t fb = 0; fb < total; fb += 128) {
+      uint32_t vv[4], pos[4];
+      bool fv[4];
 #pragma unroll
-      for (int s = 16; s >= 1; s >>= 1) {
-        uint32_t v = __shfl_sync(FULLMASK, incl, lo + s - 1);
-        if (v <= f) lo += s;
-      }
-      uint32_t o_incl = __shfl_sync(FULLMASK, incl, lo);
-      uint32_t o_d = __shfl_sync(FULLMASK, d, lo);
-      uint32_t o_st = __shfl_sync(FULLMASK, st, lo);
-      bool isnew = false;
-      uint32_t v = 0;
-      if (fv) {
-        v = g.adjV[o_st + (f - (o_incl - o_d))];
-        uint32_t old = atomicAdd(&w.slot[(size_t)v * 8], 1u);
-        isnew = (old == 0u);
-        if (bm) {
-          uint32_t pos = base + lo;
-          atomicOr(&w.slot[(size_t)v * 8 + 4 + (pos >> 5)], 1u << (pos & 31));
+      for (int j = 0; j < 4; ++j) {
+        uint32_t f = fb + 32 * j + lane;
+        fv[j] = f < total;
+        int lo = 0;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+          uint32_t v = __shfl_sync(FULLMASK, incl, lo + s - 1);
+          if (v <= f) lo += s;
         }
+        uint32_t o_incl = __shfl_sync(FULLMASK, incl, lo);
+        uint32_t o_d = __shfl_sync(FULLMASK, d, lo);
+        uint32_t o_st = __shfl_sync(FULLMASK, st, lo);
+        pos[j] = base + lo;
+        vv[j] = fv[j] ? __ldg(&g.adjV[o_st + (f - (o_incl - o_d))]) : 0u;
       }
-      uint32_t b = __ballot_sync(FULLMASK, isnew);
-      if (isnew) w.touched[nt + __popc(b & lanemask_lt())] = v;
-      nt += __popc(b);
+      uint32_t old[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * 8], 1u) : 1u;
+      if (bm) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (fv[j]) atomicOr(&w.slot[(size_t)vv[j] * 8 + 4 + (pos[j] >> 5)], 1u << (pos[j] & 31));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        bool isnew = old[j] == 0u;
+        uint32_t b = __ballot_sync(FULLMASK, isnew);
+        if (isnew) w.touched[nt + __popc(b & lanemask_lt())] = vv[j];
+        nt += __popc(b);
+      }
     }
   }
   sL = warp_sum64(sL);
@@ -646,25 +655,40 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
   bool nonmax = false;
   uint32_t nPc = 0, nQc = 0, nRx = 0;
   unsigned long long sRx = 0;
-  for (uint32_t tb = 0; tb < nt; tb += 32) {
-    uint32_t t = tb + lane;
-    bool valid = t < nt;
-    uint32_t v = valid ? w.touched[t] : 0u;
-    uint32_t c = 0;
-    uint32_t rw[4] = {0u, 0u, 0u, 0u};
-    unsigned long long tg = 0;
-    if (valid) {
-      uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)v * 8);
-      uint4 a = sp[0], b = sp[1];
-      c = a.x;
-      tg = ((unsigned long long)a.w << 32) | a.z;
-      rw[0] = b.x;
-      rw[1] = b.y;
-      rw[2] = b.z;
-      rw[3] = b.w;
-      sp[0] = make_uint4(0u, 0u, 0u, 0u);
-      sp[1] = make_uint4(0u, 0u, 0u, 0u);
+  for (uint32_t tb = 0; tb < nt; tb += 64) {
+    uint32_t vs[2];
+    uint4 sa[2], sb[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      uint32_t t = tb + 32 * j + lane;
+      vs[j] = t < nt ? w.touched[t] : 0xffffffffu;
     }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (vs[j] != 0xffffffffu) {
+        const uint4* sp = reinterpret_cast<const uint4*>(w.slot + (size_t)vs[j] * 8);
+        sa[j] = sp[0];
+        sb[j] = sp[1];
+      } else {
+        sa[j] = make_uint4(0u, 0u, 0u, 0u);
+        sb[j] = sa[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (vs[j] != 0xffffffffu) {
+        uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)vs[j] * 8);
+        sp[0] = make_uint4(0u, 0u, 0u, 0u);
+        sp[1] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+    const bool valid = vs[j] != 0xffffffffu;
+    const uint32_t v = valid ? vs[j] : 0u;
+    const uint32_t c = sa[j].x;
+    const unsigned long long tg = ((unsigned long long)sa[j].w << 32) | sa[j].z;
+    const uint32_t rw[4] = {sb[j].x, sb[j].y, sb[j].z, sb[j].w};
     // role: 0 none/R, 1 Q-role, 2 P-role
     int role = 0;
     if (valid) {
@@ -706,6 +730,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
       }
       nQc += __popc(bq);
     }
+      }
   }
   nonmax = __any_sync(FULLMASK, nonmax);
   sRx = warp_sum64(sRx);
@@ -1018,7 +1043,10 @@ __device__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t
 }
 
 // ================================================================== kernel
-__global__ void __launch_bounds__(256) mbe_search_kernel(SearchParams p) {
+#ifndef MBE_MINBLOCKS
+#define MBE_MINBLOCKS 2
+#endif
+__global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const uint32_t wib = threadIdx.x >> 5;
