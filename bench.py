@@ -341,7 +341,7 @@ def run_ours(args):
             "stats": {"tasks": st.tasks, "pruned": st.pruned, "list_tasks": st.list_tasks,
                       "bitmap_tasks": st.bitmap_tasks, "frames": st.frames, "max_depth": st.max_depth,
                       "phase_frac": [round(c / max(1, st.n_warps * st.kernel_ms * 1.965e6), 4)
-                                     for c in st.phase_cycles[:6]]},
+                                     for c in st.phase_cycles[:15]]},
         }
         print(json.dumps(line), flush=True)
     G.close()

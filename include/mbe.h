@@ -109,10 +109,14 @@ typedef struct {
   uint32_t n_warps;         /* persistent warps launched */
   uint32_t max_depth;       /* MBE_STATS: deepest stack level reached */
   /* MBE_STATS: Σ over warps of SM cycles spent per phase (the Eq. 1 breakdown, and the
-   * fetch/steal/idle shares of Fig. 6): [0] level-1 (root) tasks incl. subtree fetch,
-   * [1] list-path tasks, [2] bit-row tasks, [3] stealing (scan + claim), [4] idle backoff,
-   * [5] waiting for thieves before a pop, [6..7] reserved. */
-  uint64_t phase_cycles[8];
+   * fetch/steal/idle shares of Fig. 6).  Totals: [0] level-1 (root) tasks incl. subtree
+   * fetch, [1] list-path tasks below level 1, [2] bit-row tasks, [3] stealing (scan + claim),
+   * [4] idle backoff, [5] waiting for thieves before a pop.  Sub-phases of list-path tasks (roots
+   * included): [6] L' construction + role tags (Eq. 1 "B"), [7] reverse scan, [8] maximality check
+   * + expansion classification ("C"+"E"), [9] ordering of P' ("A"), [10] child frame build.
+   * Sub-phases of bit-row tasks: [11] maximality check, [12] expansion + emit, [13] Q' rows +
+   * ordering, [14] child frame build.  [15] reserved. */
+  uint64_t phase_cycles[16];
 } mbe_result;
 
 /* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be

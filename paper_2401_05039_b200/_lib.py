@@ -44,7 +44,7 @@ class mbe_result(ctypes.Structure):
     _fields_ = [("count", _u64), ("hash", _u64), ("tasks", _u64), ("pruned", _u64), ("steals", _u64),
                 ("records_written", _u64), ("truncated", _u32), ("candidate_side", _i32), ("kernel_ms", _dbl),
                 ("wall_ms", _dbl), ("alg_bytes", _u64), ("list_tasks", _u64), ("bitmap_tasks", _u64),
-                ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 8)]
+                ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 16)]
 
 
 class mbe_graph_info(ctypes.Structure):

@@ -563,7 +563,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     res->frames = hg.frames;
     res->n_warps = n_warps;
     res->max_depth = hg.max_depth;
-    for (int k = 0; k < 8; ++k) res->phase_cycles[k] = hg.phase[k];
+    for (int k = 0; k < 16; ++k) res->phase_cycles[k] = hg.phase[k];
     if (cfg.per_root) {
       std::vector<uint64_t> pr(4ull * S.nU);
       CUDA_TRY(cudaMemcpy(pr.data(), W->per_root.p, 32ull * S.nU, cudaMemcpyDeviceToHost));

@@ -43,7 +43,7 @@ struct Globals {
   unsigned int pad;
   unsigned long long out_records, out_ids;
   unsigned long long err_info;
-  unsigned long long phase[8];  // MBE_STATS: Σ over warps of cycles per phase (see mbe.h)
+  unsigned long long phase[16];  // MBE_STATS: Σ over warps of cycles per phase (see mbe.h)
 };
 
 struct SearchParams {

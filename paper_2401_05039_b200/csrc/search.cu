@@ -43,6 +43,7 @@ struct __align__(16) WarpSmem {
   unsigned int foff[MBE_MAXDEPTH];  // arena word offset of the frame at each depth
   unsigned int fnp[MBE_MAXDEPTH];   // its |P| (task count)
   unsigned int pend[MBE_MAXDEPTH];  // prefetched claim result (PEND_NONE = none)
+  unsigned long long ph[16];        // MBE_STATS phase cycles (lane 0), see include/mbe.h
 };
 #define PEND_NONE 0xffffffffu
 
@@ -69,7 +70,6 @@ struct Warp {
   // lane-0 accumulators
   unsigned long long count, hash, tasks, pruned, steals, list_tasks, bitmap_tasks, frames, alg_bytes;
   uint32_t max_depth;
-  unsigned long long ph[8];  // MBE_STATS phase cycles (lane 0)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -94,6 +94,16 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+// MBE_STATS sub-phase accounting: add the cycles since `t` to phase k and restart `t`.
+#define MBE_PHASE(k, t)                                              \
+  do {                                                               \
+    if ((p.flags & F_STATS) && w.lane == 0) {                        \
+      unsigned long long now_ = (unsigned long long)clock64();       \
+      w.sm->ph[k] += now_ - (t);                                     \
+      (t) = now_;                                                    \
+    }                                                                \
+  } while (0)
 
 __device__ __forceinline__ void set_error(const SearchParams& p, unsigned int code, unsigned long long info) {
   if (atomicCAS(&p.gl->error, 0u, code) == 0u) p.gl->err_info = info;
@@ -561,6 +571,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     return;
   }
 
+  unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
   // Step 2: L' = L ∩ N(x)
   const uint32_t* Lp;
   uint32_t nLp;
@@ -591,6 +602,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     __syncwarp();
   }
 
+  MBE_PHASE(6, tph);
   // Reverse scan: for u ∈ L' (position pos), for v ∈ N(u): cnt[v]++,
   // bit pos of row(v) when building a bit-row child.  Flattened over the warp.
   unsigned long long sL = 0;
@@ -651,6 +663,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
   sL = warp_sum64(sL);
   __syncwarp();
 
+  MBE_PHASE(7, tph);
   // Classification of every touched vertex (Steps 3 and 4).
   bool nonmax = false;
   uint32_t nPc = 0, nQc = 0, nRx = 0;
@@ -736,6 +749,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
   sRx = warp_sum64(sRx);
   __syncwarp();
 
+  MBE_PHASE(8, tph);
   account_task(w, p, nonmax);
   if (lane == 0 && (p.flags & F_STATS)) {
     w.list_tasks++;
@@ -752,6 +766,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
 
   // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.
   warp_sort_pairs(w, p, nPc, nLp);
+  MBE_PHASE(9, tph);
   const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (bm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
                                                             : 2ull * nPc);
   if (!arena_reserve(w, p, need)) return;
@@ -790,6 +805,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
   }
   publish_frame(w, p, size, nPc);
+  MBE_PHASE(10, tph);
 }
 
 // ================================================================== bit-row path
@@ -805,6 +821,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   const uint32_t* Prow = F + align4((uint64_t)(Pid + nP - F));
   const uint32_t* Qrow = Prow + (size_t)nP * W;
 
+  unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
   const uint32_t x = Pid[i];
   const Row<W> Lx = load_row<W>(Prow + (size_t)i * W);  // L' = row(x) (Step 2)
   uint32_t k = 0;
@@ -838,6 +855,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
       }
     }
   }
+  MBE_PHASE(11, tph);
   account_task(w, p, nonmax);
   if (lane == 0 && (p.flags & F_STATS)) {
     w.bitmap_tasks++;
@@ -886,6 +904,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, k, sRp, nRp);
 
+  MBE_PHASE(12, tph);
   const bool need_child = nPc > 0;
   if (!need_child && !p.cap_records) return;
 
@@ -920,6 +939,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   }
   __syncwarp();
   warp_sort_pairs(w, p, nPc, k);
+  MBE_PHASE(13, tph);
 
   const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (1 + Wn) + (uint64_t)nQc * Wn;
   if (!arena_reserve(w, p, need)) return;
@@ -950,6 +970,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
     if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
   }
   publish_frame(w, p, size, nPc);
+  MBE_PHASE(14, tph);
 }
 
 __device__ __forceinline__ int task_phase(const uint32_t* F) {
@@ -1077,8 +1098,9 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
   w.count = w.hash = w.tasks = w.pruned = w.steals = 0;
   w.list_tasks = w.bitmap_tasks = w.frames = w.alg_bytes = 0;
   w.max_depth = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) w.ph[k] = 0;
+  if (lane == 0)
+    for (int k = 0; k < 16; ++k) w.sm->ph[k] = 0;
+  __syncwarp();
 
   const bool steal = !(p.flags & F_NO_STEAL);
   const unsigned long long t_start = globaltimer_ns();
@@ -1110,7 +1132,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         if (lane == 0) {
           atomicAdd(&dsc->done, 1u);
           w.sm->pend[d] = (uint32_t)nxt;
-          if (p.flags & F_STATS) w.ph[task_phase(F)] += clock64() - t0;
+          if (p.flags & F_STATS) w.sm->ph[task_phase(F)] += clock64() - t0;
         }
         __syncwarp();
       } else {
@@ -1128,7 +1150,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
           atomicExch(&dsc->claim, 0ull);
           dsc->done = 0u;
           p.tops[gw] = d;
-          if (p.flags & F_STATS) w.ph[5] += clock64() - t0;
+          if (p.flags & F_STATS) w.sm->ph[5] += clock64() - t0;
         }
         w.failed = __shfl_sync(FULLMASK, (int)w.failed, 0);
         w.top = d;
@@ -1150,7 +1172,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         w.cur_root = x;
         unsigned long long t0 = stats_clock(p);
         list_task(w, p, nullptr, 0u, x);
-        if (lane == 0 && (p.flags & F_STATS)) w.ph[0] += clock64() - t0;
+        if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[0] += clock64() - t0;
         continue;
       }
       roots_done = true;
@@ -1177,11 +1199,11 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       rot += 97;
     }
     if (!got) {
-      if (lane == 0 && (p.flags & F_STATS)) w.ph[3] += clock64() - t0;
+      if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[3] += clock64() - t0;
       unsigned long long t1 = stats_clock(p);
       __nanosleep(backoff);
       if (backoff < 2048) backoff <<= 1;
-      if (lane == 0 && (p.flags & F_STATS)) w.ph[4] += clock64() - t1;
+      if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[4] += clock64() - t1;
       continue;
     }
     backoff = 64;
@@ -1190,14 +1212,14 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
     Desc* vd = p.desc + (size_t)v * MBE_MAXDEPTH + dd;
     const uint32_t off = ld_volatile(&vd->off);
     const uint32_t* F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)v * p.ws_stride + p.o_arena) + off;
-    if (lane == 0 && (p.flags & F_STATS)) w.ph[3] += clock64() - t0;
+    if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[3] += clock64() - t0;
     unsigned long long t2 = stats_clock(p);
     run_task(w, p, F, ti);
     __syncwarp();
     if (lane == 0) {
       w.steals++;
       atomicAdd(&vd->done, 1u);
-      if (p.flags & F_STATS) w.ph[task_phase(F)] += clock64() - t2;
+      if (p.flags & F_STATS) w.sm->ph[task_phase(F)] += clock64() - t2;
     }
   }
 
@@ -1215,7 +1237,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       atomicAdd(&p.gl->frames, w.frames);
       atomicAdd(&p.gl->alg_bytes, w.alg_bytes);
       atomicMax(&p.gl->max_depth, w.max_depth);
-      for (int k = 0; k < 8; ++k) atomicAdd(&p.gl->phase[k], w.ph[k]);
+      for (int k = 0; k < 16; ++k) atomicAdd(&p.gl->phase[k], w.sm->ph[k]);
     }
   }
 }
