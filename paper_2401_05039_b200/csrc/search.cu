@@ -221,7 +221,7 @@ __device__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, 
   __syncwarp();
 }
 
-__device__ __noinline__ void sort_smem(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
+__device__ void sort_smem(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
   uint32_t N = 64;
   while (N < n) N <<= 1;
   for (uint32_t t = lane; t < N; t += 32) {
@@ -256,7 +256,7 @@ __device__ __noinline__ void sort_smem(unsigned long long* key, uint32_t* val, u
 
 // Stable LSD radix sort with 8-bit digits over the significant bits of
 // key = (count << 32) | id.  Ping-pong between (key,val) and (key2,val2).
-__device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, unsigned long long* key2, uint32_t* val2,
+__device__ void sort_radix(unsigned long long* key, uint32_t* val, unsigned long long* key2, uint32_t* val2,
                            uint32_t n, uint32_t id_bits, uint32_t cnt_bits, WarpSmem* sm, int lane) {
   unsigned long long* src_k = key;
   uint32_t* src_v = val;
@@ -329,7 +329,7 @@ __device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, 
 
 __device__ __forceinline__ uint32_t bit_length(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
 
-__device__ __noinline__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint32_t max_count) {
+__device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint32_t max_count) {
   if (n <= 1) return;
   if (n <= 32) {
     sort_regs32(w.skey, w.sval, n, w.lane);
@@ -349,7 +349,7 @@ __device__ __noinline__ void warp_sort_pairs(Warp& w, const SearchParams& p, uin
 // "∃q: L'' ⊆ N(q)" holds for a dominated row only if it holds for its
 // dominator.  With keep_all, rows are copied unchanged.
 template <int W>
-__device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane) {
+__device__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane) {
   if (keep_all) {
     for (uint32_t t = lane; t < n; t += 32) store_row<W>(dst + (size_t)t * W, load_row<W>(src + (size_t)t * W));
     __syncwarp();
@@ -421,7 +421,7 @@ __device__ __forceinline__ bool bsearch_u32(const uint32_t* a, uint32_t n, uint3
 }
 
 // out = A ∩ B (both sorted ascending), in ascending order; returns |out|.
-__device__ __noinline__ uint32_t warp_intersect(const uint32_t* A, uint32_t nA, const uint32_t* B, uint32_t nB, uint32_t* out,
+__device__ uint32_t warp_intersect(const uint32_t* A, uint32_t nA, const uint32_t* B, uint32_t nB, uint32_t* out,
                                    int lane) {
   if (nA > nB) {
     const uint32_t* t = A;
@@ -473,7 +473,7 @@ __device__ __forceinline__ void account_emit(Warp& w, const SearchParams& p, uin
 
 // Bounded listing: record (A, B) in original ids.  Lids: L' (V ids) sorted;
 // R' = Rfr (frame R, U ranks) ∪ {x} ∪ rexp (U ranks).
-__device__ __noinline__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lids, uint32_t nL, const uint32_t* Rfr,
+__device__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lids, uint32_t nL, const uint32_t* Rfr,
                              uint32_t nRf, uint32_t x, const uint32_t* rexp, uint32_t nRx) {
   uint32_t nR = nRf + 1 + nRx;
   unsigned long long rec = 0, ido = 0;
@@ -541,7 +541,7 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
 // ================================================================== list path
 // Task x on a list frame F (or the implicit root frame when F == nullptr:
 // L = V, R = ∅, Q-role = ranks < x, P-role = ranks > x).
-__device__ __noinline__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i, uint32_t xroot) {
+__device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i, uint32_t xroot) {
   const DevGraph& g = p.g;
   const int lane = w.lane;
   const bool root = (F == nullptr);
@@ -810,7 +810,7 @@ __device__ __noinline__ void list_task(Warp& w, const SearchParams& p, const uin
 
 // ================================================================== bit-row path
 template <int W>
-__device__ __noinline__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+__device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
   const DevGraph& g = p.g;
   const int lane = w.lane;
   const uint32_t nL = F[1], nP = F[2], nQ = F[3], nR = F[4];
@@ -998,7 +998,7 @@ __device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p)
 // advertised by the hint bitmap, scanning circularly from gw+1,
 // and claim ONE task of the bottom-most such frame (largest subtree).
 // Returns true with (*victim, *depth, *task) on success.
-__device__ __noinline__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t* victim, uint32_t* depth,
+__device__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t* victim, uint32_t* depth,
                           uint32_t* task) {
   const int lane = w.lane;
   const uint32_t nw = (p.n_warps + 31) >> 5;
