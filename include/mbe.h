@@ -68,7 +68,7 @@ typedef struct {
   uint32_t struct_size;      /* ABI versioning: sizeof(mbe_config) */
   uint32_t ctas_per_sm;      /* persistent CTAs per SM; 0 = auto */
   uint32_t threads_per_cta;  /* multiple of 32, <= 1024; 0 = auto */
-  uint32_t bitmap_threshold; /* frames with |L| <= this use bit rows (<= 128); 0 = auto */
+  uint32_t bitmap_threshold; /* frames with |L| <= this use bit rows (<= 512); 0 = auto (largest that fits) */
   int32_t candidate_side;    /* 0 = auto (smaller side, ties: side 1), 1 = rows, 2 = cols; result-invariant */
   uint32_t flags;            /* MBE_* flags above */
   uint32_t rank, world;      /* this process' share of the level-1 subtrees (world >= 1) */

@@ -196,6 +196,21 @@ int build_side(mbe_graph* g, int s) {
 
 uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
+// Per-warp workspace bytes (same layout as checkout_workspace).
+uint64_t workspace_stride(uint64_t nU, uint64_t maxdeg, uint64_t arena_bytes, uint32_t wmax) {
+  nU = std::max<uint64_t>(nU, 1);
+  const uint64_t lb = std::max<uint64_t>(maxdeg, 32 * MBE_WMAX);
+  uint64_t o = align256(nU * 4 * MBE_SLOT_WORDS);
+  o = align256(o + nU * 4);
+  o = align256(o + lb * 4);
+  o = align256(o + nU * 4);
+  o = align256(o + nU * 16);
+  o = align256(o + nU * 8);
+  o = align256(o + nU * wmax * 4);
+  o = align256(o + nU * wmax * 4);
+  return align256(o + arena_bytes);
+}
+
 // Check out a workspace able to run n_warps warps over nU candidate vertices.
 int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t maxdeg, uint64_t arena_bytes,
                        uint32_t wmax, Workspace** out) {
@@ -219,7 +234,7 @@ int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t maxde
   w->cap_lbuf = lb;
   w->arena_bytes = arena_bytes;
   uint64_t o = 0;
-  w->o_slot = o; o = align256(o + nU * 32);
+  w->o_slot = o; o = align256(o + nU * 4 * MBE_SLOT_WORDS);
   w->o_touched = o; o = align256(o + nU * 4);
   w->o_lbuf = o; o = align256(o + lb * 4);
   w->o_rbuf = o; o = align256(o + nU * 4);
@@ -411,7 +426,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   }
   if (cfg.world == 0 || cfg.rank >= cfg.world) return fail(MBE_EINVAL, "rank/world");
   if (cfg.threads_per_cta % 32 || cfg.threads_per_cta > 256) return fail(MBE_EINVAL, "threads_per_cta must be a multiple of 32 <= 256");
-  if (cfg.bitmap_threshold > 32 * MBE_WMAX) return fail(MBE_EINVAL, "bitmap_threshold > 128");
+  if (cfg.bitmap_threshold > 32 * MBE_WMAX) return fail(MBE_EINVAL, "bitmap_threshold > 512");
   if (cfg.candidate_side < 0 || cfg.candidate_side > 2) return fail(MBE_EINVAL, "candidate_side");
   if (out && (out->cap_records && (!out->rec_off || !out->rec_n1 || !out->rec_n2)))
     return fail(MBE_EINVAL, "mbe_output buffers");
@@ -430,14 +445,32 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   }
   const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : 256;
   const uint32_t ctas_per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 2;
-  const uint32_t T = cfg.bitmap_threshold ? cfg.bitmap_threshold : 128;
-  const uint32_t wmax = mbe_words_for(T);
   const uint32_t grid = (uint32_t)g->sm_count * ctas_per_sm;
   const uint32_t n_warps = grid * (threads / 32);
   // auto arena: proportional to the graph, 256 KiB .. 8 MiB per warp; grown x4 and retried on overflow
   uint64_t arena = cfg.arena_bytes ? cfg.arena_bytes
                                    : std::min<uint64_t>(8ull << 20, std::max<uint64_t>(256ull << 10, 16ull * (S.nU + S.nV + g->nE)));
   arena = (arena + 255) & ~255ull;
+  // auto bit-row threshold: the widest rows (512 columns) whose workspace fits in 60% of free memory
+  uint32_t T = cfg.bitmap_threshold;
+  if (!T) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    uint64_t pooled = 0;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      for (Workspace* w : g_pool)
+        if (!w->busy && w->device == g->device) pooled += w->ws.bytes;
+    }
+    T = 128;
+    for (uint32_t t : {512u, 256u}) {
+      if ((double)workspace_stride(S.nU, S.maxdegU, arena, mbe_words_for(t)) * n_warps <= 0.6 * (double)(fr + pooled)) {
+        T = t;
+        break;
+      }
+    }
+  }
+  const uint32_t wmax = mbe_words_for(T);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cfg.stream);
 
   // listing buffers (device) for this call

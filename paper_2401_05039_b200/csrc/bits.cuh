@@ -104,5 +104,7 @@ MBE_HD void mbe_compress_apply_w(const MbeCompress<W>& c, const uint32_t* x, uin
   }
 }
 
-// Words per bit row for a frame with n columns (1, 2 or 4).
-MBE_HD uint32_t mbe_words_for(uint32_t n) { return n <= 32 ? 1u : (n <= 64 ? 2u : 4u); }
+// Words per bit row for a frame with n columns (1, 2, 4, 8 or 16).
+MBE_HD uint32_t mbe_words_for(uint32_t n) {
+  return n <= 32 ? 1u : (n <= 64 ? 2u : (n <= 128 ? 4u : (n <= 256 ? 8u : 16u)));
+}

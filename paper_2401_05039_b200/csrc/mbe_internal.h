@@ -4,7 +4,8 @@
 #include <stdint.h>
 
 #define MBE_MAXDEPTH 128   // per-warp stack depth (search depth is 7-11 on C2-C5)
-#define MBE_WMAX 4         // bit rows of up to 4 x 32 = 128 columns
+#define MBE_WMAX 16        // bit rows of up to 16 x 32 = 512 columns
+#define MBE_SLOT_WORDS 24  // per-vertex scratch slot: count, -, tag (2), bit row (16), pad (4) = 96 B
 #define MBE_SMEM_SORT 256  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
 #define MBE_HDR_WORDS 8    // frame header
 
@@ -49,7 +50,7 @@ struct Globals {
 struct SearchParams {
   DevGraph g;
   int cand_side;  // 1 or 2 (A/B orientation of the hash)
-  uint32_t T;     // bitmap threshold (<= 32 * MBE_WMAX)
+  uint32_t T;     // bitmap threshold (<= 32 * MBE_WMAX = 512)
   uint32_t flags;
   uint32_t rank, world;
   unsigned long long* claim_counter;  // NULL -> static deal

@@ -44,13 +44,15 @@ struct __align__(16) WarpSmem {
   unsigned int fnp[MBE_MAXDEPTH];   // its |P| (task count)
   unsigned int pend[MBE_MAXDEPTH];  // prefetched claim result (PEND_NONE = none)
   unsigned long long ph[16];        // MBE_STATS phase cycles (lane 0), see include/mbe.h
+  unsigned int lx[MBE_WMAX];        // row(x) of a wide (8/16-word) bit-row task
+  unsigned short posv[32 * MBE_WMAX];  // column positions of row(x)'s set bits (wide compression)
 };
 #define PEND_NONE 0xffffffffu
 
 struct Warp {
   int lane;
   uint32_t gw;
-  uint32_t* slot;  // [nU][8]: cnt, -, tag lo, tag hi, bits[4] (one 32-byte sector per vertex)
+  uint32_t* slot;  // [nU][MBE_SLOT_WORDS]: cnt, -, tag lo, tag hi, bits[16], pad (first sector: cnt, tag, bits 0-3)
   uint32_t* touched;
   uint32_t* lbuf;
   uint32_t* rbuf;
@@ -401,11 +403,84 @@ __device__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bo
   return K;
 }
 
+// Same reduction for wide rows (8 or 16 words), word-sliced: rows are streamed from
+// memory (L1) instead of held in registers.
+__device__ __forceinline__ bool wide_subset(const uint32_t* a, const uint32_t* b, uint32_t W) {  // a ⊆ b
+  uint32_t x = 0;
+  for (uint32_t q = 0; q < W; ++q) x |= a[q] & ~b[q];
+  return x == 0;
+}
+__device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, uint32_t W) {
+  uint32_t x = 0;
+  for (uint32_t q = 0; q < W; ++q) x |= a[q] ^ b[q];
+  return x == 0;
+}
+
+__device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* dst, uint32_t W, bool keep_all,
+                                   int lane) {
+  if (keep_all) {
+    for (uint32_t t = lane; t < n * W; t += 32) dst[t] = src[t];
+    __syncwarp();
+    return n;
+  }
+  uint32_t K = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t t = base + lane;
+    const bool valid = t < n;
+    const uint32_t* r = src + (size_t)(valid ? t : 0) * W;
+    bool dom = !valid;
+    for (uint32_t k = 0; k < K && !dom; ++k)
+      if (wide_subset(r, dst + (size_t)k * W, W)) dom = true;
+    const uint32_t cnt = min(32u, n - base);
+    for (uint32_t m = 0; m < cnt && !dom; ++m) {
+      if ((int)m == lane) continue;
+      const uint32_t* mr = src + (size_t)(base + m) * W;
+      if (wide_subset(r, mr, W) && ((int)m < lane || !wide_eq(r, mr, W))) dom = true;
+    }
+    const bool surv = valid && !dom;
+    const uint32_t bs = __ballot_sync(FULLMASK, surv);
+    if (bs) {
+      uint32_t newK = 0;
+      for (uint32_t kb = 0; kb < K; kb += 32) {
+        const bool kval = kb + lane < K;
+        const uint32_t* kr = dst + (size_t)(kval ? kb + lane : 0) * W;
+        bool kdom = false;
+        uint32_t rem = bs;
+        while (rem && kval && !kdom) {
+          const int m = __ffs(rem) - 1;
+          rem &= rem - 1;
+          if (wide_subset(kr, src + (size_t)(base + m) * W, W)) kdom = true;
+        }
+        const bool keep = kval && !kdom;
+        uint32_t row[MBE_WMAX];
+        for (uint32_t q = 0; q < W; ++q) row[q] = keep ? kr[q] : 0u;
+        const uint32_t bk = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) {
+          uint32_t* o = dst + (size_t)(newK + __popc(bk & lanemask_lt())) * W;
+          for (uint32_t q = 0; q < W; ++q) o[q] = row[q];
+        }
+        newK += __popc(bk);
+        __syncwarp();
+      }
+      K = newK;
+      if (surv) {
+        uint32_t* o = dst + (size_t)(K + __popc(bs & lanemask_lt())) * W;
+        for (uint32_t q = 0; q < W; ++q) o[q] = r[q];
+      }
+      K += __popc(bs);
+      __syncwarp();
+    }
+  }
+  return K;
+}
+
 __device__ __forceinline__ uint32_t antichain_w(uint32_t Wc, const uint32_t* src, uint32_t n, uint32_t* dst,
                                                 bool keep_all, int lane) {
   if (Wc == 1) return antichain<1>(src, n, dst, keep_all, lane);
   if (Wc == 2) return antichain<2>(src, n, dst, keep_all, lane);
-  return antichain<4>(src, n, dst, keep_all, lane);
+  if (Wc == 4) return antichain<4>(src, n, dst, keep_all, lane);
+  return antichain_wide(src, n, dst, Wc, keep_all, lane);
 }
 
 // ------------------------------------------------------------------ misc
@@ -596,9 +671,9 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     w.stamp++;
     const unsigned long long st = ((unsigned long long)w.stamp) << 32;
     for (uint32_t j = lane; j < nP; j += 32)
-      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)Pid[j] * 8 + 2) = st | (j + 1);
+      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)Pid[j] * MBE_SLOT_WORDS + 2) = st | (j + 1);
     for (uint32_t j = lane; j < nR; j += 32)
-      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)R[j] * 8 + 2) = st | TAG_R;
+      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)R[j] * MBE_SLOT_WORDS + 2) = st | TAG_R;
     __syncwarp();
   }
 
@@ -645,11 +720,11 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
       }
       uint32_t old[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * 8], 1u) : 1u;
+      for (int j = 0; j < 4; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
       if (bm) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (fv[j]) atomicOr(&w.slot[(size_t)vv[j] * 8 + 4 + (pos[j] >> 5)], 1u << (pos[j] & 31));
+          if (fv[j]) atomicOr(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + (pos[j] >> 5)], 1u << (pos[j] & 31));
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -679,7 +754,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       if (vs[j] != 0xffffffffu) {
-        const uint4* sp = reinterpret_cast<const uint4*>(w.slot + (size_t)vs[j] * 8);
+        const uint4* sp = reinterpret_cast<const uint4*>(w.slot + (size_t)vs[j] * MBE_SLOT_WORDS);
         sa[j] = sp[0];
         sb[j] = sp[1];
       } else {
@@ -690,7 +765,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       if (vs[j] != 0xffffffffu) {
-        uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)vs[j] * 8);
+        uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)vs[j] * MBE_SLOT_WORDS);
         sp[0] = make_uint4(0u, 0u, 0u, 0u);
         sp[1] = make_uint4(0u, 0u, 0u, 0u);
       }
@@ -727,21 +802,28 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
     nRx += __popc(be);
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
+    // words 4.. of a wide (8/16-word) row are still in the slot: copied, then cleared below
+    uint32_t* ex = w.slot + (size_t)v * MBE_SLOT_WORDS + 8;
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
       w.skey[idx] = ((unsigned long long)c << 32) | v;
       w.sval[idx] = idx;
-      if (bm)
-        for (uint32_t q = 0; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
+      if (bm) {
+        for (uint32_t q = 0; q < Wc && q < 4; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
+        for (uint32_t q = 4; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = ex[q - 4];
+      }
     }
     nPc += __popc(bp);
     if (bm) {
       uint32_t bq = __ballot_sync(FULLMASK, isQ);
       if (isQ) {
         uint32_t idx = nQc + __popc(bq & lanemask_lt());
-        for (uint32_t q = 0; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = rw[q];
+        for (uint32_t q = 0; q < Wc && q < 4; ++q) w.qbuf[(size_t)idx * Wc + q] = rw[q];
+        for (uint32_t q = 4; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = ex[q - 4];
       }
       nQc += __popc(bq);
+      if (Wc > 4 && valid)
+        for (uint32_t q = 4; q < Wc; ++q) ex[q - 4] = 0u;
     }
       }
   }
@@ -973,6 +1055,191 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   MBE_PHASE(14, tph);
 }
 
+// ================================================================== wide bit-row path
+// Frames with 128 < |L| <= 512 (8 or 16 words per row).  Same steps as
+// bitmap_task, word-sliced: row(x) lives in shared memory, every other row is
+// streamed from memory (L1) one word at a time, and child rows are column-
+// compressed by ballot transposition (lane l gathers column posv[32c + l]).
+__device__ void bitmap_task_wide(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+  const DevGraph& g = p.g;
+  const int lane = w.lane;
+  const uint32_t W = (F[0] >> 8) & 0xffu;
+  const uint32_t nL = F[1], nP = F[2], nQ = F[3], nR = F[4];
+  const uint64_t sR = *reinterpret_cast<const unsigned long long*>(F + 6);
+  const uint32_t* L = F + MBE_HDR_WORDS;
+  const uint32_t* R = L + nL;
+  const uint32_t* Pid = R + nR;
+  const uint32_t* Prow = F + align4((uint64_t)(Pid + nP - F));
+  const uint32_t* Qrow = Prow + (size_t)nP * W;
+  unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+
+  const uint32_t x = Pid[i];
+  uint32_t* lx = w.sm->lx;
+  if (lane < (int)W) lx[lane] = Prow[(size_t)i * W + lane];
+  __syncwarp();
+  const uint32_t k = __reduce_add_sync(FULLMASK, lane < (int)W ? (uint32_t)__popc(lx[lane]) : 0u);
+
+  // Step 3: (a) identical earlier sibling in the equal-key block (R2), (b) Q rows ⊇ row(x)
+  bool nonmax = false;
+  for (uint32_t cb = 0; cb < i; cb += 32) {
+    const int j = (int)i - 1 - (int)cb - lane;
+    const bool valid = j >= 0;
+    bool eq = valid;
+    uint32_t pk = 0;
+    if (valid) {
+      const uint32_t* r = Prow + (size_t)j * W;
+      for (uint32_t q = 0; q < W; ++q) {
+        const uint32_t a = r[q];
+        pk += __popc(a);
+        eq &= a == lx[q];
+      }
+    }
+    if (__any_sync(FULLMASK, eq)) {
+      nonmax = true;
+      break;
+    }
+    if (__any_sync(FULLMASK, !valid || pk < k)) break;
+  }
+  if (!nonmax) {
+    for (uint32_t qb = 0; qb < nQ; qb += 32) {
+      const bool valid = qb + lane < nQ;
+      bool sub = valid;
+      if (valid) {
+        const uint32_t* r = Qrow + (size_t)(qb + lane) * W;
+        for (uint32_t q = 0; q < W; ++q) sub &= (lx[q] & ~r[q]) == 0u;
+      }
+      if (__any_sync(FULLMASK, sub)) {
+        nonmax = true;
+        break;
+      }
+    }
+  }
+  MBE_PHASE(11, tph);
+  account_task(w, p, nonmax);
+  if (lane == 0 && (p.flags & F_STATS)) {
+    w.bitmap_tasks++;
+    w.alg_bytes += 4ull * W * (1ull + nP + nQ) + 4ull * nP;
+  }
+  if (nonmax) return;
+
+  // Step 4: expansion over P-role rows j > i (pbuf keeps the source row index of each P' candidate)
+  uint32_t nPc = 0, nRx = 0, nQc = 0;
+  unsigned long long sRx = 0;
+  for (uint32_t jb = i + 1; jb < nP; jb += 32) {
+    const uint32_t j = jb + lane;
+    const bool valid = j < nP;
+    uint32_t c = 0;
+    if (valid) {
+      const uint32_t* r = Prow + (size_t)j * W;
+      for (uint32_t q = 0; q < W; ++q) c += __popc(r[q] & lx[q]);
+    }
+    const uint32_t v = valid ? Pid[j] : 0u;
+    const bool isExp = valid && c == k;
+    const bool isPc = valid && c > 0 && c < k;
+    if (isExp) sRx += g.hvU[v];
+    const uint32_t be = __ballot_sync(FULLMASK, isExp);
+    if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
+    nRx += __popc(be);
+    const uint32_t bp = __ballot_sync(FULLMASK, isPc);
+    if (isPc) {
+      const uint32_t idx = nPc + __popc(bp & lanemask_lt());
+      w.skey[idx] = ((unsigned long long)c << 32) | v;
+      w.sval[idx] = idx;
+      w.pbuf[idx] = j;
+    }
+    nPc += __popc(bp);
+  }
+  sRx = warp_sum64(sRx);
+  // L' ids and column positions of row(x), in ascending order
+  unsigned long long sL = 0;
+  uint32_t before = 0;
+  for (uint32_t q = 0; q < W; ++q) {
+    const uint32_t word = lx[q];
+    const bool bit = (word >> lane) & 1u;
+    const uint32_t rank = before + __popc(word & lanemask_lt());
+    if (bit) {
+      const uint32_t id = L[q * 32 + lane];
+      sL += g.hvV[id];
+      w.lbuf[rank] = id;
+      w.sm->posv[rank] = (unsigned short)(q * 32 + lane);
+    }
+    before += __popc(word);
+  }
+  sL = warp_sum64(sL);
+  __syncwarp();
+  const uint32_t nRp = nR + 1 + nRx;
+  const uint64_t sRp = sR + g.hvU[x] + sRx;
+  account_emit(w, p, sL, k, sRp, nRp);
+  if (p.cap_records) write_record(w, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
+  MBE_PHASE(12, tph);
+  if (nPc == 0) return;
+
+  // Q' candidates: Q rows and Q-role siblings P[j<i] meeting L'; qbuf keeps source row pointers
+  for (uint32_t qb = 0; qb < nQ + i; qb += 32) {
+    const uint32_t t = qb + lane;
+    const bool valid = t < nQ + i;
+    bool keep = false;
+    uint32_t off = 0;
+    if (valid) {
+      off = t < nQ ? (uint32_t)((Qrow - F) + (size_t)t * W) : (uint32_t)((Prow - F) + (size_t)(t - nQ) * W);
+      const uint32_t* r = F + off;
+      uint32_t a = 0;
+      for (uint32_t q = 0; q < W; ++q) a |= r[q] & lx[q];
+      keep = a != 0u;
+    }
+    const uint32_t bq = __ballot_sync(FULLMASK, keep);
+    if (keep) w.qbuf[nQc + __popc(bq & lanemask_lt())] = off;
+    nQc += __popc(bq);
+  }
+  __syncwarp();
+  warp_sort_pairs(w, p, nPc, k);
+  MBE_PHASE(13, tph);
+
+  const uint32_t Wn = mbe_words_for(k);
+  const uint64_t need = MBE_HDR_WORDS + k + nRp + 8 + (uint64_t)nPc * (1 + Wn) + 2ull * nQc * Wn;
+  if (!arena_reserve(w, p, need)) return;
+  uint32_t* C = w.arena + w.atop;
+  uint32_t* CL = C + MBE_HDR_WORDS;
+  uint32_t* CR = CL + k;
+  uint32_t* CP = CR + nRp;
+  for (uint32_t t = lane; t < k; t += 32) CL[t] = w.lbuf[t];
+  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
+  uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
+  // ballot-transposed column compression of one source row into Wn words
+  auto compress_row = [&](const uint32_t* src, uint32_t* dst) {
+    for (uint32_t c = 0; c < Wn; ++c) {
+      const uint32_t pidx = c * 32 + lane;
+      uint32_t bit = 0;
+      if (pidx < k) {
+        const uint32_t pos = w.sm->posv[pidx];
+        bit = (src[pos >> 5] >> (pos & 31)) & 1u;
+      }
+      const uint32_t word = __ballot_sync(FULLMASK, bit != 0u);
+      if (lane == 0) dst[c] = word;
+    }
+  };
+  for (uint32_t t = 0; t < nPc; ++t) compress_row(Prow + (size_t)w.pbuf[w.sval[t]] * W, CPr + (size_t)t * Wn);
+  uint32_t* CQ = CPr + (size_t)nPc * Wn;
+  uint32_t* scratch = CQ + (size_t)nQc * Wn;  // compressed Q' candidates, reduced into CQ below
+  for (uint32_t t = 0; t < nQc; ++t) compress_row(F + w.qbuf[t], scratch + (size_t)t * Wn);
+  __syncwarp();
+  const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane);
+  const uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
+  if (lane == 0) {
+    C[0] = KIND_BITMAP | (Wn << 8);
+    C[1] = k;
+    C[2] = nPc;
+    C[3] = nQk;
+    C[4] = nRp;
+    C[5] = w.cur_root;
+    *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
+    if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
+  }
+  publish_frame(w, p, size, nPc);
+  MBE_PHASE(14, tph);
+}
+
 __device__ __forceinline__ int task_phase(const uint32_t* F) {
   return (F[0] & 0xffu) == KIND_LIST ? 1 : 2;
 }
@@ -986,7 +1253,8 @@ __device__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint
     const uint32_t W = (h >> 8) & 0xffu;
     if (W == 1) bitmap_task<1>(w, p, F, i);
     else if (W == 2) bitmap_task<2>(w, p, F, i);
-    else bitmap_task<4>(w, p, F, i);
+    else if (W == 4) bitmap_task<4>(w, p, F, i);
+    else bitmap_task_wide(w, p, F, i);
   }
 }
 

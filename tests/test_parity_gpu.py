@@ -97,12 +97,23 @@ def test_random_mid_graphs_both_sides(n, p):
 
 
 # ------------------------------------------------------------------ result invariance under every knob
-@pytest.mark.parametrize("T", [32, 64, 128])
+@pytest.mark.parametrize("T", [32, 64, 128, 256, 512])
 @pytest.mark.parametrize("flags", [0, MBE_NO_STEAL, MBE_NO_ANTICHAIN | MBE_NO_TWIN, MBE_STATS])
 def test_knobs_do_not_change_result_or_tree(T, flags):
     g = I.erdos_renyi_c1b()
     want = oracle.mbea(g)
     assert same(gpu(g, bitmap_threshold=T, flags=flags), want)
+
+
+@pytest.mark.parametrize("g", [I.random_bipartite(12, 400, 0.7, 1), I.random_bipartite(20, 300, 0.5, 2),
+                               I.random_bipartite(300, 16, 0.6, 3), I.random_bipartite(40, 700, 0.3, 4)],
+                         ids=lambda g: g.name)
+@pytest.mark.parametrize("T", [128, 256, 512])
+def test_wide_bit_rows(g, T):
+    """Frames with 128 < |L| <= 512 use 8/16-word rows (list path above T); tree and result unchanged."""
+    want = oracle.mbea(g)
+    assert same(gpu(g, bitmap_threshold=T), want)
+    assert same(gpu(g, bitmap_threshold=T, flags=MBE_NO_ANTICHAIN), want)
 
 
 @pytest.mark.parametrize("ctas,threads", [(1, 32), (1, 256), (2, 128), (4, 64)])
