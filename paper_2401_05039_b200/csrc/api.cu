@@ -81,7 +81,7 @@ struct Workspace {
   bool busy = false, dirty = true;
   uint32_t n_warps = 0, wmax = 0;
   uint64_t cap_nU = 0, cap_lbuf = 0, arena_bytes = 0, stride = 0;
-  uint64_t o_slot = 0, o_touched = 0, o_lbuf = 0, o_rbuf = 0, o_skey = 0, o_sval = 0, o_pbuf = 0, o_qbuf = 0,
+  uint64_t o_slot = 0, o_sext = 0, o_touched = 0, o_lbuf = 0, o_rbuf = 0, o_skey = 0, o_sval = 0, o_pbuf = 0, o_qbuf = 0,
            o_arena = 0;
   DevBuf ws, desc, tops, stamps, hint, per_root, gl;
   void release() {
@@ -201,6 +201,7 @@ uint64_t workspace_stride(uint64_t nU, uint64_t maxdeg, uint64_t arena_bytes, ui
   nU = std::max<uint64_t>(nU, 1);
   const uint64_t lb = std::max<uint64_t>(maxdeg, 32 * MBE_WMAX);
   uint64_t o = align256(nU * 4 * MBE_SLOT_WORDS);
+  o = align256(o + nU * 4 * MBE_SEXT_WORDS);
   o = align256(o + nU * 4);
   o = align256(o + lb * 4);
   o = align256(o + nU * 4);
@@ -235,6 +236,7 @@ int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t maxde
   w->arena_bytes = arena_bytes;
   uint64_t o = 0;
   w->o_slot = o; o = align256(o + nU * 4 * MBE_SLOT_WORDS);
+  w->o_sext = o; o = align256(o + nU * 4 * MBE_SEXT_WORDS);
   w->o_touched = o; o = align256(o + nU * 4);
   w->o_lbuf = o; o = align256(o + lb * 4);
   w->o_rbuf = o; o = align256(o + nU * 4);
@@ -536,6 +538,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.ws = static_cast<uint8_t*>(W->ws.p);
     p.ws_stride = W->stride;
     p.o_slot = W->o_slot;
+    p.o_sext = W->o_sext;
     p.o_touched = W->o_touched;
     p.o_lbuf = W->o_lbuf;
     p.o_rbuf = W->o_rbuf;

@@ -52,7 +52,8 @@ struct __align__(16) WarpSmem {
 struct Warp {
   int lane;
   uint32_t gw;
-  uint32_t* slot;  // [nU][MBE_SLOT_WORDS]: cnt, -, tag lo, tag hi, bits[16], pad (first sector: cnt, tag, bits 0-3)
+  uint32_t* slot;  // [nU][MBE_SLOT_WORDS]: cnt, -, tag lo, tag hi, bit row words 0-3 (one 32-B sector)
+  uint32_t* sext;  // [nU][MBE_SEXT_WORDS]: bit row words 4-15 (wide rows)
   uint32_t* touched;
   uint32_t* lbuf;
   uint32_t* rbuf;
@@ -416,8 +417,24 @@ __device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, ui
   return x == 0;
 }
 
+// Wide-row antichain with cheap necessary-condition filters: a ⊆ b requires
+// popc(a) <= popc(b) and fold(a) ⊆ fold(b), fold = OR of the words.  Kept-row
+// (popc, fold) pairs live in shared memory (first 256 kept rows).
+__device__ __forceinline__ unsigned long long wide_meta(const uint32_t* r, uint32_t W) {
+  uint32_t pc = 0, f = 0;
+  for (uint32_t q = 0; q < W; ++q) {
+    const uint32_t a = r[q];
+    pc += __popc(a);
+    f |= a;
+  }
+  return ((unsigned long long)pc << 32) | f;
+}
+__device__ __forceinline__ bool meta_may_subset(unsigned long long a, unsigned long long b) {
+  return (a >> 32) <= (b >> 32) && ((uint32_t)a & ~(uint32_t)b) == 0u;
+}
+
 __device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* dst, uint32_t W, bool keep_all,
-                                   int lane) {
+                                   int lane, unsigned long long* kmeta /* smem [MBE_SMEM_SORT] */) {
   if (keep_all) {
     for (uint32_t t = lane; t < n * W; t += 32) dst[t] = src[t];
     __syncwarp();
@@ -428,14 +445,19 @@ __device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* ds
     const uint32_t t = base + lane;
     const bool valid = t < n;
     const uint32_t* r = src + (size_t)(valid ? t : 0) * W;
+    const unsigned long long mr = valid ? wide_meta(r, W) : 0ull;
     bool dom = !valid;
-    for (uint32_t k = 0; k < K && !dom; ++k)
-      if (wide_subset(r, dst + (size_t)k * W, W)) dom = true;
-    const uint32_t cnt = min(32u, n - base);
-    for (uint32_t m = 0; m < cnt && !dom; ++m) {
-      if ((int)m == lane) continue;
-      const uint32_t* mr = src + (size_t)(base + m) * W;
-      if (wide_subset(r, mr, W) && ((int)m < lane || !wide_eq(r, mr, W))) dom = true;
+    for (uint32_t k = 0; k < K; ++k) {
+      const unsigned long long mk = k < MBE_SMEM_SORT ? kmeta[k] : wide_meta(dst + (size_t)k * W, W);
+      if (!dom && meta_may_subset(mr, mk) && wide_subset(r, dst + (size_t)k * W, W)) dom = true;
+    }
+    const uint32_t vb = __ballot_sync(FULLMASK, valid);
+    for (int m = 0; m < 32; ++m) {
+      const unsigned long long mm = __shfl_sync(FULLMASK, mr, m);
+      if (!dom && ((vb >> m) & 1u) && m != lane && meta_may_subset(mr, mm)) {
+        const uint32_t* o = src + (size_t)(base + m) * W;
+        if (wide_subset(r, o, W) && (m < lane || !wide_eq(r, o, W))) dom = true;
+      }
     }
     const bool surv = valid && !dom;
     const uint32_t bs = __ballot_sync(FULLMASK, surv);
@@ -443,13 +465,15 @@ __device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* ds
       uint32_t newK = 0;
       for (uint32_t kb = 0; kb < K; kb += 32) {
         const bool kval = kb + lane < K;
-        const uint32_t* kr = dst + (size_t)(kval ? kb + lane : 0) * W;
+        const uint32_t kk = kval ? kb + lane : 0u;
+        const uint32_t* kr = dst + (size_t)kk * W;
+        const unsigned long long mk = kval ? (kk < MBE_SMEM_SORT ? kmeta[kk] : wide_meta(kr, W)) : 0ull;
         bool kdom = false;
-        uint32_t rem = bs;
-        while (rem && kval && !kdom) {
-          const int m = __ffs(rem) - 1;
-          rem &= rem - 1;
-          if (wide_subset(kr, src + (size_t)(base + m) * W, W)) kdom = true;
+        for (int m = 0; m < 32; ++m) {
+          const unsigned long long ms = __shfl_sync(FULLMASK, mr, m);
+          if (((bs >> m) & 1u) && kval && !kdom && meta_may_subset(mk, ms) &&
+              wide_subset(kr, src + (size_t)(base + m) * W, W))
+            kdom = true;
         }
         const bool keep = kval && !kdom;
         uint32_t row[MBE_WMAX];
@@ -457,16 +481,20 @@ __device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* ds
         const uint32_t bk = __ballot_sync(FULLMASK, keep);
         __syncwarp();
         if (keep) {
-          uint32_t* o = dst + (size_t)(newK + __popc(bk & lanemask_lt())) * W;
+          const uint32_t ni = newK + __popc(bk & lanemask_lt());
+          uint32_t* o = dst + (size_t)ni * W;
           for (uint32_t q = 0; q < W; ++q) o[q] = row[q];
+          if (ni < MBE_SMEM_SORT) kmeta[ni] = mk;
         }
         newK += __popc(bk);
         __syncwarp();
       }
       K = newK;
       if (surv) {
-        uint32_t* o = dst + (size_t)(K + __popc(bs & lanemask_lt())) * W;
+        const uint32_t ni = K + __popc(bs & lanemask_lt());
+        uint32_t* o = dst + (size_t)ni * W;
         for (uint32_t q = 0; q < W; ++q) o[q] = r[q];
+        if (ni < MBE_SMEM_SORT) kmeta[ni] = mr;
       }
       K += __popc(bs);
       __syncwarp();
@@ -476,11 +504,11 @@ __device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* ds
 }
 
 __device__ __forceinline__ uint32_t antichain_w(uint32_t Wc, const uint32_t* src, uint32_t n, uint32_t* dst,
-                                                bool keep_all, int lane) {
+                                                bool keep_all, int lane, WarpSmem* sm) {
   if (Wc == 1) return antichain<1>(src, n, dst, keep_all, lane);
   if (Wc == 2) return antichain<2>(src, n, dst, keep_all, lane);
   if (Wc == 4) return antichain<4>(src, n, dst, keep_all, lane);
-  return antichain_wide(src, n, dst, Wc, keep_all, lane);
+  return antichain_wide(src, n, dst, Wc, keep_all, lane, sm->skey);
 }
 
 // ------------------------------------------------------------------ misc
@@ -724,7 +752,12 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
       if (bm) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (fv[j]) atomicOr(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + (pos[j] >> 5)], 1u << (pos[j] & 31));
+          if (fv[j]) {
+            const uint32_t q = pos[j] >> 5;
+            uint32_t* wd = q < 4 ? &w.slot[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + q]
+                                 : &w.sext[(size_t)vv[j] * MBE_SEXT_WORDS + q - 4];
+            atomicOr(wd, 1u << (pos[j] & 31));
+          }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -803,7 +836,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     nRx += __popc(be);
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
     // words 4.. of a wide (8/16-word) row are still in the slot: copied, then cleared below
-    uint32_t* ex = w.slot + (size_t)v * MBE_SLOT_WORDS + 8;
+    uint32_t* ex = w.sext + (size_t)v * MBE_SEXT_WORDS;
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
       w.skey[idx] = ((unsigned long long)c << 32) | v;
@@ -869,7 +902,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     }
     uint32_t* CQ = CPr + (size_t)nPc * Wc;
     __syncwarp();
-    nQk = antichain_w(Wc, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane);
+    nQk = antichain_w(Wc, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
     size = (uint64_t)(CQ + (size_t)nQk * Wc - C);
   } else {
     uint32_t* CK = CP + nPc;
@@ -1039,7 +1072,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   }
   uint32_t* CQ = CPr + (size_t)nPc * Wn;
   __syncwarp();
-  uint32_t nQk = antichain_w(Wn, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane);
+  uint32_t nQk = antichain_w(Wn, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
   uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
@@ -1224,7 +1257,7 @@ __device__ void bitmap_task_wide(Warp& w, const SearchParams& p, const uint32_t*
   uint32_t* scratch = CQ + (size_t)nQc * Wn;  // compressed Q' candidates, reduced into CQ below
   for (uint32_t t = 0; t < nQc; ++t) compress_row(F + w.qbuf[t], scratch + (size_t)t * Wn);
   __syncwarp();
-  const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane);
+  const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
   const uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
@@ -1347,6 +1380,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
   w.gw = gw;
   uint8_t* base = p.ws + (size_t)gw * p.ws_stride;
   w.slot = reinterpret_cast<uint32_t*>(base + p.o_slot);
+  w.sext = reinterpret_cast<uint32_t*>(base + p.o_sext);
   w.touched = reinterpret_cast<uint32_t*>(base + p.o_touched);
   w.lbuf = reinterpret_cast<uint32_t*>(base + p.o_lbuf);
   w.rbuf = reinterpret_cast<uint32_t*>(base + p.o_rbuf);
