@@ -526,6 +526,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.g.maxdegU = S.maxdegU;
     p.cand_side = side;
     p.T = T;
+    {
+      const char* q = std::getenv("MBE_WIDE_QCAP");
+      p.wide_qcap = q ? (uint32_t)std::strtoul(q, nullptr, 10) : 1024u;
+    }
     p.flags = cfg.flags;
     p.rank = cfg.rank;
     p.world = cfg.world;

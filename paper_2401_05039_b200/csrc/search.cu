@@ -879,10 +879,13 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
   if (p.cap_records) write_record(w, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
   if (nPc == 0) return;
 
-  // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.
+  // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.  A wide (8/16-word)
+  // bit-row child is built only when its Q' is small (p.wide_qcap), since one warp builds it
+  // serially; otherwise the child stays a list frame (implicit Q is exact either way).
+  const bool cbm = bm && (Wc <= 4 || nQc <= p.wide_qcap);
   warp_sort_pairs(w, p, nPc, nLp);
   MBE_PHASE(9, tph);
-  const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (bm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
+  const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
                                                             : 2ull * nPc);
   if (!arena_reserve(w, p, need)) return;
   uint32_t* C = w.arena + w.atop;
@@ -894,7 +897,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
   for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
   uint64_t size;
   uint32_t nQk = 0;
-  if (bm) {
+  if (cbm) {
     uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
     for (uint32_t t = lane; t < nPc; t += 32) {
       uint32_t src = w.sval[t];
@@ -910,7 +913,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
     size = (uint64_t)(CK + nPc - C);
   }
   if (lane == 0) {
-    C[0] = (bm ? KIND_BITMAP : KIND_LIST) | (Wc << 8);
+    C[0] = (cbm ? KIND_BITMAP : KIND_LIST) | ((cbm ? Wc : 0u) << 8);
     C[1] = nLp;
     C[2] = nPc;
     C[3] = nQk;
