@@ -52,7 +52,8 @@ struct SearchParams {
   DevGraph g;
   int cand_side;  // 1 or 2 (A/B orientation of the hash)
   uint32_t T;     // bitmap threshold (<= 32 * MBE_WMAX = 512)
-  uint32_t wide_qcap;  // max Q' candidates for relocalizing a list task's child into 8/16-word rows
+  uint32_t wide_qcap;   // relocalize a list task's child into 8/16-word rows if |Q'| <= wide_qcap
+  uint32_t wide_ratio;  //   ... or |Q'| <= wide_ratio * |P'|
   uint32_t flags;
   uint32_t rank, world;
   unsigned long long* claim_counter;  // NULL -> static deal
