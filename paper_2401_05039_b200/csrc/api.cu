@@ -528,7 +528,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.T = T;
     {
       const char* q = std::getenv("MBE_WIDE_QCAP");
-      p.wide_qcap = q ? (uint32_t)std::strtoul(q, nullptr, 10) : 1024u;
+      p.wide_qcap = q ? (uint32_t)std::strtoul(q, nullptr, 10) : 256u;
       const char* r = std::getenv("MBE_WIDE_RATIO");
       p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 16u;
     }

@@ -36,6 +36,9 @@
 
 namespace {
 
+#define SM_PROW_WORDS 256
+#define SM_QROW_WORDS 512
+#define SM_RBUF 128
 struct __align__(16) WarpSmem {
   unsigned long long skey[MBE_SMEM_SORT];
   unsigned int sval[MBE_SMEM_SORT];
@@ -46,8 +49,14 @@ struct __align__(16) WarpSmem {
   unsigned long long ph[16];        // MBE_STATS phase cycles (lane 0), see include/mbe.h
   unsigned int lx[MBE_WMAX];        // row(x) of a wide (8/16-word) bit-row task
   unsigned short posv[32 * MBE_WMAX];  // column positions of row(x)'s set bits (wide compression)
+  // shared-memory scratch of narrow bit-row tasks whose candidate bounds are small (the common case)
+  unsigned int prow[SM_PROW_WORDS];  // compressed P' candidate rows
+  unsigned int qrow[SM_QROW_WORDS];  // compressed Q' candidate rows
+  unsigned int lbuf[128];            // L' ids
+  unsigned int rbuf[SM_RBUF];        // expanded R' vertices
 };
 #define PEND_NONE 0xffffffffu
+#define SM_KEPT_WORDS (MBE_SMEM_SORT * 2)  // antichain kept list staged in skey's storage
 
 struct Warp {
   int lane;
@@ -331,6 +340,12 @@ __device__ void sort_radix(unsigned long long* key, uint32_t* val, unsigned long
 }
 
 __device__ __forceinline__ uint32_t bit_length(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
+
+__device__ void sort_pairs_small(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
+  if (n <= 1) return;
+  if (n <= 32) sort_regs32(key, val, n, lane);
+  else sort_smem(key, val, n, sm, lane);
+}
 
 __device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint32_t max_count) {
   if (n <= 1) return;
@@ -644,7 +659,7 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
 // ================================================================== list path
 // Task x on a list frame F (or the implicit root frame when F == nullptr:
 // L = V, R = ∅, Q-role = ranks < x, P-role = ranks > x).
-__device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i, uint32_t xroot) {
+__device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i, uint32_t xroot) {
   const DevGraph& g = p.g;
   const int lane = w.lane;
   const bool root = (F == nullptr);
@@ -929,7 +944,7 @@ __device__ void list_task(Warp& w, const SearchParams& p, const uint32_t* F, uin
 
 // ================================================================== bit-row path
 template <int W>
-__device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+__device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
   const DevGraph& g = p.g;
   const int lane = w.lane;
   const uint32_t nL = F[1], nP = F[2], nQ = F[3], nR = F[4];
@@ -987,6 +1002,16 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   const MbeCompress<W> cmp = mbe_compress_prep_w<W>(Lx.w);
   uint32_t nPc = 0, nRx = 0, nQc = 0;
   unsigned long long sRx = 0;
+  // scratch in shared memory when the candidate bounds fit (P' <= nP-i-1, Q' <= nQ+i)
+  const uint32_t maxP = nP - i - 1, maxQ = nQ + i;
+  const bool smP = maxP <= MBE_SMEM_SORT && maxP * Wn <= SM_PROW_WORDS && maxP <= SM_RBUF;
+  const bool smQ = maxQ * Wn <= SM_QROW_WORDS;
+  unsigned long long* kbuf = smP ? w.sm->skey : w.skey;
+  uint32_t* vbuf = smP ? w.sm->sval : w.sval;
+  uint32_t* pbuf = smP ? w.sm->prow : w.pbuf;
+  uint32_t* rbuf = smP ? w.sm->rbuf : w.rbuf;
+  uint32_t* qbuf = smQ ? w.sm->qrow : w.qbuf;
+  uint32_t* lbuf = w.sm->lbuf;
   for (uint32_t jb = i + 1; jb < nP; jb += 32) {
     uint32_t j = jb + lane;
     bool valid = j < nP;
@@ -997,16 +1022,16 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
     bool isPc = valid && c > 0 && c < k;
     if (isExp) sRx += g.hvU[v];
     uint32_t be = __ballot_sync(FULLMASK, isExp);
-    if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
+    if (isExp) rbuf[nRx + __popc(be & lanemask_lt())] = v;
     nRx += __popc(be);
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
-      w.skey[idx] = ((unsigned long long)c << 32) | v;
-      w.sval[idx] = idx;
+      kbuf[idx] = ((unsigned long long)c << 32) | v;
+      vbuf[idx] = idx;
       uint32_t out[4];
       mbe_compress_apply_w<W>(cmp, r.w, out);
-      for (uint32_t q = 0; q < Wn; ++q) w.pbuf[(size_t)idx * Wn + q] = out[q];
+      for (uint32_t q = 0; q < Wn; ++q) pbuf[(size_t)idx * Wn + q] = out[q];
     }
     nPc += __popc(bp);
   }
@@ -1034,10 +1059,10 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
     uint32_t b = Lx.w[q];
     uint32_t before = 0;
     for (int qq = 0; qq < q; ++qq) before += __popc(Lx.w[qq]);
-    if (bit) w.lbuf[before + __popc(b & lanemask_lt())] = L[q * 32 + lane];
+    if (bit) lbuf[before + __popc(b & lanemask_lt())] = L[q * 32 + lane];
   }
   __syncwarp();
-  if (p.cap_records) write_record(w, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
+  if (p.cap_records) write_record(w, p, lbuf, k, R, nR, x, rbuf, nRx);
   if (!need_child) return;
 
   // Q' candidates: frame Q rows and Q-role siblings P[j<i] meeting L'
@@ -1052,12 +1077,13 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
       uint32_t idx = nQc + __popc(bq & lanemask_lt());
       uint32_t out[4];
       mbe_compress_apply_w<W>(cmp, r.w, out);
-      for (uint32_t q = 0; q < Wn; ++q) w.qbuf[(size_t)idx * Wn + q] = out[q];
+      for (uint32_t q = 0; q < Wn; ++q) qbuf[(size_t)idx * Wn + q] = out[q];
     }
     nQc += __popc(bq);
   }
   __syncwarp();
-  warp_sort_pairs(w, p, nPc, k);
+  if (smP) sort_pairs_small(kbuf, vbuf, nPc, w.sm, lane);
+  else warp_sort_pairs(w, p, nPc, k);
   MBE_PHASE(13, tph);
 
   const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (1 + Wn) + (uint64_t)nQc * Wn;
@@ -1066,17 +1092,25 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
   uint32_t* CL = C + MBE_HDR_WORDS;
   uint32_t* CR = CL + k;
   uint32_t* CP = CR + nRp;
-  for (uint32_t t = lane; t < k; t += 32) CL[t] = w.lbuf[t];
-  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
-  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
+  for (uint32_t t = lane; t < k; t += 32) CL[t] = lbuf[t];
+  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : rbuf[t - nR - 1]);
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)kbuf[t];
   uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
   for (uint32_t t = lane; t < nPc; t += 32) {
-    uint32_t src = w.sval[t];
-    for (uint32_t q = 0; q < Wn; ++q) CPr[(size_t)t * Wn + q] = w.pbuf[(size_t)src * Wn + q];
+    uint32_t src = vbuf[t];
+    for (uint32_t q = 0; q < Wn; ++q) CPr[(size_t)t * Wn + q] = pbuf[(size_t)src * Wn + q];
   }
   uint32_t* CQ = CPr + (size_t)nPc * Wn;
   __syncwarp();
-  uint32_t nQk = antichain_w(Wn, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+  uint32_t nQk;
+  if (nQc * Wn <= SM_KEPT_WORDS && !(p.flags & F_NO_ANTICHAIN)) {
+    // reduce into shared memory (skey storage is free again), then copy the survivors out
+    uint32_t* kept = reinterpret_cast<uint32_t*>(w.sm->skey);
+    nQk = antichain_w(Wn, qbuf, nQc, kept, false, lane, w.sm);
+    for (uint32_t t = lane; t < nQk * Wn; t += 32) CQ[t] = kept[t];
+  } else {
+    nQk = antichain_w(Wn, qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+  }
   uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
@@ -1097,7 +1131,7 @@ __device__ void bitmap_task(Warp& w, const SearchParams& p, const uint32_t* F, u
 // bitmap_task, word-sliced: row(x) lives in shared memory, every other row is
 // streamed from memory (L1) one word at a time, and child rows are column-
 // compressed by ballot transposition (lane l gathers column posv[32c + l]).
-__device__ void bitmap_task_wide(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+__device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
   const DevGraph& g = p.g;
   const int lane = w.lane;
   const uint32_t W = (F[0] >> 8) & 0xffu;
@@ -1281,7 +1315,7 @@ __device__ __forceinline__ int task_phase(const uint32_t* F) {
   return (F[0] & 0xffu) == KIND_LIST ? 1 : 2;
 }
 
-__device__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+__device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
   const uint32_t h = F[0];
   w.cur_root = F[5];
   if ((h & 0xffu) == KIND_LIST) {
