@@ -36,9 +36,10 @@
 
 namespace {
 
-#define SM_PROW_WORDS 256
-#define SM_QROW_WORDS 512
+#define SM_PROW_WORDS 128
+#define SM_QROW_WORDS 256
 #define SM_RBUF 128
+#define FC_WORDS 640  // shared-memory copy of the warp's top frame (owner reads only)
 struct __align__(16) WarpSmem {
   unsigned long long skey[MBE_SMEM_SORT];
   unsigned int sval[MBE_SMEM_SORT];
@@ -47,11 +48,17 @@ struct __align__(16) WarpSmem {
   unsigned int fnp[MBE_MAXDEPTH];   // its |P| (task count)
   unsigned int pend[MBE_MAXDEPTH];  // prefetched claim result (PEND_NONE = none)
   unsigned long long ph[16];        // MBE_STATS phase cycles (lane 0), see include/mbe.h
-  unsigned int lx[MBE_WMAX];        // row(x) of a wide (8/16-word) bit-row task
-  unsigned short posv[32 * MBE_WMAX];  // column positions of row(x)'s set bits (wide compression)
-  // shared-memory scratch of narrow bit-row tasks whose candidate bounds are small (the common case)
-  unsigned int prow[SM_PROW_WORDS];  // compressed P' candidate rows
-  unsigned int qrow[SM_QROW_WORDS];  // compressed Q' candidate rows
+  unsigned int fcache[FC_WORDS];     // copy of the frame at depth fc_depth (16-B aligned)
+  unsigned int fsz[MBE_MAXDEPTH];    // frame size in words per depth
+  int fc_depth;                      // depth held in fcache, -1 = none
+  unsigned int lx[MBE_WMAX];         // row(x) of a wide (8/16-word) bit-row task
+  union {
+    unsigned short posv[32 * MBE_WMAX];  // wide tasks: column positions of row(x)'s set bits
+    struct {                             // narrow tasks with small candidate bounds:
+      unsigned int prow[SM_PROW_WORDS];  //   compressed P' candidate rows
+      unsigned int qrow[SM_QROW_WORDS];  //   compressed Q' candidate rows
+    };
+  };
   unsigned int lbuf[128];            // L' ids
   unsigned int rbuf[SM_RBUF];        // expanded R' vertices
 };
@@ -644,6 +651,8 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
     w.sm->foff[w.top] = (unsigned int)w.atop;
     w.sm->fnp[w.top] = nP;
     w.sm->pend[w.top] = PEND_NONE;
+    w.sm->fsz[w.top] = (unsigned int)size_words;
+    if (w.sm->fc_depth == (int)w.top) w.sm->fc_depth = -1;
     __threadfence();
     atomicExch(&d->claim, ((unsigned long long)nP) << 32);
     p.tops[w.gw] = w.top + 1;
@@ -1438,8 +1447,10 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
   w.count = w.hash = w.tasks = w.pruned = w.steals = 0;
   w.list_tasks = w.bitmap_tasks = w.frames = w.alg_bytes = 0;
   w.max_depth = 0;
-  if (lane == 0)
+  if (lane == 0) {
     for (int k = 0; k < 16; ++k) w.sm->ph[k] = 0;
+    w.sm->fc_depth = -1;
+  }
   __syncwarp();
 
   const bool steal = !(p.flags & F_NO_STEAL);
@@ -1466,6 +1477,17 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         unsigned long long nxt = PEND_NONE;
         if (lane == 0) nxt = (i + 1 < nP) ? atomicAdd(&dsc->claim, 1ull) : (unsigned long long)nP;
         const uint32_t* F = w.arena + w.sm->foff[d];
+        const uint32_t fsz = w.sm->fsz[d];
+        if (fsz <= FC_WORDS) {
+          if (w.sm->fc_depth != (int)d) {  // (re)load the top frame into shared memory
+            const uint4* src = reinterpret_cast<const uint4*>(F);
+            uint4* dst = reinterpret_cast<uint4*>(w.sm->fcache);
+            for (uint32_t t = lane; t < (fsz + 3) / 4; t += 32) dst[t] = src[t];
+            __syncwarp();
+            if (lane == 0) w.sm->fc_depth = (int)d;
+          }
+          F = w.sm->fcache;
+        }
         unsigned long long t0 = stats_clock(p);
         run_task(w, p, F, i);
         __syncwarp();
@@ -1495,6 +1517,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         w.failed = __shfl_sync(FULLMASK, (int)w.failed, 0);
         w.top = d;
         w.atop = w.sm->foff[d];
+        if (lane == 0 && w.sm->fc_depth == (int)d) w.sm->fc_depth = -1;
         __syncwarp();
       }
       continue;
