@@ -40,7 +40,7 @@ namespace {
 #define SM_QROW_WORDS 256
 #define SM_RBUF 128
 #define FC_WORDS 640  // shared-memory copy of the warp's top frame (owner reads only)
-struct __align__(16) WarpSmem {
+struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligned offset
   unsigned long long skey[MBE_SMEM_SORT];
   unsigned int sval[MBE_SMEM_SORT];
   unsigned int hist[256];
@@ -50,9 +50,10 @@ struct __align__(16) WarpSmem {
   unsigned long long ph[16];        // MBE_STATS phase cycles (lane 0), see include/mbe.h
   unsigned int fcache[FC_WORDS];     // copy of the frame at depth fc_depth (16-B aligned)
   unsigned int fsz[MBE_MAXDEPTH];    // frame size in words per depth
-  int fc_depth;                      // depth held in fcache, -1 = none
   unsigned int lx[MBE_WMAX];         // row(x) of a wide (8/16-word) bit-row task
-  union {
+  int fc_depth;                      // depth held in fcache, -1 = none
+  int pad_[3];
+  union __align__(16) {
     unsigned short posv[32 * MBE_WMAX];  // wide tasks: column positions of row(x)'s set bits
     struct {                             // narrow tasks with small candidate bounds:
       unsigned int prow[SM_PROW_WORDS];  //   compressed P' candidate rows
