@@ -241,7 +241,7 @@ __device__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, 
   __syncwarp();
 }
 
-__device__ void sort_smem(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
+__device__ __noinline__ void sort_smem(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
   uint32_t N = 64;
   while (N < n) N <<= 1;
   for (uint32_t t = lane; t < N; t += 32) {
@@ -276,7 +276,7 @@ __device__ void sort_smem(unsigned long long* key, uint32_t* val, uint32_t n, Wa
 
 // Stable LSD radix sort with 8-bit digits over the significant bits of
 // key = (count << 32) | id.  Ping-pong between (key,val) and (key2,val2).
-__device__ void sort_radix(unsigned long long* key, uint32_t* val, unsigned long long* key2, uint32_t* val2,
+__device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, unsigned long long* key2, uint32_t* val2,
                            uint32_t n, uint32_t id_bits, uint32_t cnt_bits, WarpSmem* sm, int lane) {
   unsigned long long* src_k = key;
   uint32_t* src_v = val;
@@ -375,7 +375,7 @@ __device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint
 // "∃q: L'' ⊆ N(q)" holds for a dominated row only if it holds for its
 // dominator.  With keep_all, rows are copied unchanged.
 template <int W>
-__device__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane) {
+__device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane) {
   if (keep_all) {
     for (uint32_t t = lane; t < n; t += 32) store_row<W>(dst + (size_t)t * W, load_row<W>(src + (size_t)t * W));
     __syncwarp();
@@ -456,7 +456,7 @@ __device__ __forceinline__ bool meta_may_subset(unsigned long long a, unsigned l
   return (a >> 32) <= (b >> 32) && ((uint32_t)a & ~(uint32_t)b) == 0u;
 }
 
-__device__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* dst, uint32_t W, bool keep_all,
+__device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* dst, uint32_t W, bool keep_all,
                                    int lane, unsigned long long* kmeta /* smem [MBE_SMEM_SORT] */) {
   if (keep_all) {
     for (uint32_t t = lane; t < n * W; t += 32) dst[t] = src[t];
@@ -547,7 +547,7 @@ __device__ __forceinline__ bool bsearch_u32(const uint32_t* a, uint32_t n, uint3
 }
 
 // out = A ∩ B (both sorted ascending), in ascending order; returns |out|.
-__device__ uint32_t warp_intersect(const uint32_t* A, uint32_t nA, const uint32_t* B, uint32_t nB, uint32_t* out,
+__device__ __noinline__ uint32_t warp_intersect(const uint32_t* A, uint32_t nA, const uint32_t* B, uint32_t nB, uint32_t* out,
                                    int lane) {
   if (nA > nB) {
     const uint32_t* t = A;
@@ -1325,7 +1325,13 @@ __device__ __forceinline__ int task_phase(const uint32_t* F) {
   return (F[0] & 0xffu) == KIND_LIST ? 1 : 2;
 }
 
-__device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
+__device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i,
+                                         uint32_t xroot) {
+  if (F == nullptr) {  // level-1 subtree of xroot: implicit root frame
+    w.cur_root = xroot;
+    list_task(w, p, nullptr, 0u, xroot);
+    return;
+  }
   const uint32_t h = F[0];
   w.cur_root = F[5];
   if ((h & 0xffu) == KIND_LIST) {
@@ -1347,11 +1353,10 @@ __device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p)
 // advertised by the hint bitmap, scanning circularly from gw+1,
 // and claim ONE task of the bottom-most such frame (largest subtree).
 // Returns true with (*victim, *depth, *task) on success.
-__device__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t* victim, uint32_t* depth,
-                          uint32_t* task) {
-  const int lane = w.lane;
+__device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const SearchParams& p, uint32_t rot,
+                                       uint32_t* victim, uint32_t* depth, uint32_t* task) {
   const uint32_t nw = (p.n_warps + 31) >> 5;
-  const uint32_t start = ((w.gw + 1 + rot) % p.n_warps) >> 5;
+  const uint32_t start = ((gw + 1 + rot) % p.n_warps) >> 5;
   int probes = 0;
   for (uint32_t kb = 0; kb < nw && probes < 8; kb += 32) {
     uint32_t k = kb + lane;
@@ -1366,7 +1371,7 @@ __device__ bool try_steal(Warp& w, const SearchParams& p, uint32_t rot, uint32_t
         int b = __ffs(bitsv) - 1;
         bitsv &= bitsv - 1;
         uint32_t v = wi * 32 + b;
-        if (v == w.gw || v >= p.n_warps) continue;
+        if (v == gw || v >= p.n_warps) continue;
         ++probes;
         for (int attempt = 0; attempt < 2; ++attempt) {
           uint32_t tp = ld_volatile(&p.tops[v]);
@@ -1462,11 +1467,19 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
   uint32_t rot = 0;
 
   while (!w.failed) {
+    // Pick the next job, then run it at the ONE task call site below (keeps the kernel's
+    // instruction footprint small: every task body is inlined exactly once).
+    const uint32_t* F = nullptr;  // nullptr: level-1 (root) task of xr
+    uint32_t ti = 0, xr = 0, d = 0;
+    int kind = 0;                 // 1 owner, 2 root, 3 stolen
+    Desc* dsc = nullptr;
+    unsigned long long nxt = PEND_NONE;
+    unsigned long long t0 = stats_clock(p);
     if (w.top > 0) {
       // ---- owner: next task of the top frame (claims go through the shared cursor so
       // thieves can take siblings; the next claim is prefetched while this task runs)
-      const uint32_t d = w.top - 1;
-      Desc* dsc = &w.desc[d];
+      d = w.top - 1;
+      dsc = &w.desc[d];
       uint32_t i = 0;
       if (lane == 0) {
         i = w.sm->pend[d];
@@ -1474,33 +1487,8 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       }
       i = __shfl_sync(FULLMASK, i, 0);
       const uint32_t nP = w.sm->fnp[d];
-      if (i < nP) {
-        unsigned long long nxt = PEND_NONE;
-        if (lane == 0) nxt = (i + 1 < nP) ? atomicAdd(&dsc->claim, 1ull) : (unsigned long long)nP;
-        const uint32_t* F = w.arena + w.sm->foff[d];
-        const uint32_t fsz = w.sm->fsz[d];
-        if (fsz <= FC_WORDS) {
-          if (w.sm->fc_depth != (int)d) {  // (re)load the top frame into shared memory
-            const uint4* src = reinterpret_cast<const uint4*>(F);
-            uint4* dst = reinterpret_cast<uint4*>(w.sm->fcache);
-            for (uint32_t t = lane; t < (fsz + 3) / 4; t += 32) dst[t] = src[t];
-            __syncwarp();
-            if (lane == 0) w.sm->fc_depth = (int)d;
-          }
-          F = w.sm->fcache;
-        }
-        unsigned long long t0 = stats_clock(p);
-        run_task(w, p, F, i);
-        __syncwarp();
-        if (lane == 0) {
-          atomicAdd(&dsc->done, 1u);
-          w.sm->pend[d] = (uint32_t)nxt;
-          if (p.flags & F_STATS) w.sm->ph[task_phase(F)] += clock64() - t0;
-        }
-        __syncwarp();
-      } else {
+      if (i >= nP) {
         // exhausted: wait for thieves still reading it, then pop
-        unsigned long long t0 = stats_clock(p);
         if (lane == 0) {
           while (ld_volatile(&dsc->done) < nP) {
             if (ld_volatile(&p.gl->error) || globaltimer_ns() - t_start > p.watchdog_ns) {
@@ -1514,77 +1502,96 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
           dsc->done = 0u;
           p.tops[gw] = d;
           if (p.flags & F_STATS) w.sm->ph[5] += clock64() - t0;
+          if (w.sm->fc_depth == (int)d) w.sm->fc_depth = -1;
         }
         w.failed = __shfl_sync(FULLMASK, (int)w.failed, 0);
         w.top = d;
         w.atop = w.sm->foff[d];
-        if (lane == 0 && w.sm->fc_depth == (int)d) w.sm->fc_depth = -1;
         __syncwarp();
+        continue;
       }
-      continue;
-    }
-    // ---- empty stack: next level-1 subtree (coarse-grained task)
-    if (!roots_done) {
+      if (lane == 0) nxt = (i + 1 < nP) ? atomicAdd(&dsc->claim, 1ull) : (unsigned long long)nP;
+      F = w.arena + w.sm->foff[d];
+      const uint32_t fsz = w.sm->fsz[d];
+      if (fsz <= FC_WORDS) {
+        if (w.sm->fc_depth != (int)d) {  // (re)load the top frame into shared memory
+          const uint4* src = reinterpret_cast<const uint4*>(F);
+          uint4* dst = reinterpret_cast<uint4*>(w.sm->fcache);
+          for (uint32_t t = lane; t < (fsz + 3) / 4; t += 32) dst[t] = src[t];
+          __syncwarp();
+          if (lane == 0) w.sm->fc_depth = (int)d;
+        }
+        F = w.sm->fcache;
+      }
+      ti = i;
+      kind = 1;
+    } else if (!roots_done) {
+      // ---- empty stack: next level-1 subtree (coarse-grained task)
       unsigned long long pos = 0;
       if (lane == 0) {
         if (p.claim_counter) pos = atomicAdd(p.claim_counter, 1ull);
         else pos = atomicAdd(&p.gl->root_cursor, 1ull) * p.world + p.rank;
       }
       pos = __shfl_sync(FULLMASK, pos, 0);
-      if (pos < p.g.n_roots) {
-        const uint32_t x = p.g.root_order[pos];
-        w.cur_root = x;
-        unsigned long long t0 = stats_clock(p);
-        list_task(w, p, nullptr, 0u, x);
-        if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[0] += clock64() - t0;
+      if (pos >= p.g.n_roots) {
+        roots_done = true;
         continue;
       }
-      roots_done = true;
-    }
-    // ---- idle: register, then steal single tasks or terminate
-    unsigned long long t0 = stats_clock(p);
-    if (!registered) {
-      if (lane == 0) atomicAdd(&p.gl->idle, 1u);
-      registered = true;
-    }
-    uint32_t stop = 0;
-    if (lane == 0) {
-      stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
-      if (!stop && globaltimer_ns() - t_start > p.watchdog_ns) {
-        set_error(p, 4u, 0ull);  // watchdog: never hang the device
-        stop = 1;
+      xr = p.g.root_order[pos];
+      kind = 2;
+    } else {
+      // ---- idle: register, then steal single tasks or terminate
+      if (!registered) {
+        if (lane == 0) atomicAdd(&p.gl->idle, 1u);
+        registered = true;
       }
+      uint32_t stop = 0;
+      if (lane == 0) {
+        stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
+        if (!stop && globaltimer_ns() - t_start > p.watchdog_ns) {
+          set_error(p, 4u, 0ull);  // watchdog: never hang the device
+          stop = 1;
+        }
+      }
+      if (__shfl_sync(FULLMASK, stop, 0)) break;
+      uint32_t v = 0, vdep = 0;
+      bool got = false;
+      if (steal) {
+        got = try_steal(lane, gw, p, rot, &v, &vdep, &ti);  // leaves the idle set only on a successful claim
+        rot += 97;
+      }
+      if (!got) {
+        if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[3] += clock64() - t0;
+        unsigned long long t1 = stats_clock(p);
+        __nanosleep(backoff);
+        if (backoff < 2048) backoff <<= 1;
+        if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[4] += clock64() - t1;
+        continue;
+      }
+      backoff = 64;
+      registered = false;
+      __threadfence();  // acquire: the victim published the frame before its claim word
+      dsc = p.desc + (size_t)v * MBE_MAXDEPTH + vdep;
+      const uint32_t off = ld_volatile(&dsc->off);
+      F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)v * p.ws_stride + p.o_arena) + off;
+      if (lane == 0 && (p.flags & F_STATS)) {
+        const unsigned long long now = clock64();
+        w.sm->ph[3] += now - t0;
+        t0 = now;
+      }
+      kind = 3;
     }
-    if (__shfl_sync(FULLMASK, stop, 0)) break;
-    uint32_t v = 0, dd = 0, ti = 0;
-    bool got = false;
-    if (steal) {
-      got = try_steal(w, p, rot, &v, &dd, &ti);  // leaves the idle set only on a successful claim
-      rot += 97;
-    }
-    if (!got) {
-      if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[3] += clock64() - t0;
-      unsigned long long t1 = stats_clock(p);
-      __nanosleep(backoff);
-      if (backoff < 2048) backoff <<= 1;
-      if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[4] += clock64() - t1;
-      continue;
-    }
-    backoff = 64;
-    registered = false;
-    __threadfence();  // acquire: the victim published the frame before its claim word
-    Desc* vd = p.desc + (size_t)v * MBE_MAXDEPTH + dd;
-    const uint32_t off = ld_volatile(&vd->off);
-    const uint32_t* F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)v * p.ws_stride + p.o_arena) + off;
-    if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[3] += clock64() - t0;
-    unsigned long long t2 = stats_clock(p);
-    run_task(w, p, F, ti);
+
+    run_task(w, p, F, ti, xr);  // the single task call site
+
     __syncwarp();
     if (lane == 0) {
-      w.steals++;
-      atomicAdd(&vd->done, 1u);
-      if (p.flags & F_STATS) w.sm->ph[task_phase(F)] += clock64() - t2;
+      if (kind != 2) atomicAdd(&dsc->done, 1u);
+      if (kind == 1) w.sm->pend[d] = (uint32_t)nxt;
+      if (kind == 3) w.steals++;
+      if (p.flags & F_STATS) w.sm->ph[kind == 2 ? 0 : task_phase(F)] += clock64() - t0;
     }
+    __syncwarp();
   }
 
   // flush lane-0 accumulators
