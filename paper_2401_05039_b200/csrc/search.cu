@@ -47,6 +47,9 @@ struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligne
   unsigned int foff[MBE_MAXDEPTH];  // arena word offset of the frame at each depth
   unsigned int fnp[MBE_MAXDEPTH];   // its |P| (task count)
   unsigned int pend[MBE_MAXDEPTH];  // prefetched claim result (PEND_NONE = none)
+  unsigned int pendk[MBE_MAXDEPTH]; // size of the prefetched claim
+  unsigned int bcur[MBE_MAXDEPTH];  // owner's claimed batch [bcur, bend) at each depth
+  unsigned int bend[MBE_MAXDEPTH];
   unsigned long long ph[16];        // MBE_STATS phase cycles (lane 0), see include/mbe.h
   unsigned int fcache[FC_WORDS];     // copy of the frame at depth fc_depth (16-B aligned)
   unsigned int fsz[MBE_MAXDEPTH];    // frame size in words per depth
@@ -652,6 +655,8 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
     w.sm->foff[w.top] = (unsigned int)w.atop;
     w.sm->fnp[w.top] = nP;
     w.sm->pend[w.top] = PEND_NONE;
+    w.sm->bcur[w.top] = 0u;
+    w.sm->bend[w.top] = 0u;
     w.sm->fsz[w.top] = (unsigned int)size_words;
     if (w.sm->fc_depth == (int)w.top) w.sm->fc_depth = -1;
     __threadfence();
@@ -1345,6 +1350,11 @@ __device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const u
   }
 }
 
+// Owner batch size from the number of tasks not yet claimed by it (an upper bound).
+__device__ __forceinline__ uint32_t claim_batch(uint32_t rem) {
+  return rem >= 64u ? 8u : (rem >= 16u ? 4u : (rem >= 6u ? 2u : 1u));
+}
+
 __device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p) {
   return (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
 }
@@ -1480,13 +1490,29 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       // thieves can take siblings; the next claim is prefetched while this task runs)
       d = w.top - 1;
       dsc = &w.desc[d];
+      const uint32_t nP = w.sm->fnp[d];
+      // owner claims batches of up to 8 tasks per atomic (fewer L2 round trips); unclaimed
+      // tasks stay stealable.  The next batch is prefetched while the batch's last task runs.
       uint32_t i = 0;
       if (lane == 0) {
-        i = w.sm->pend[d];
-        if (i == PEND_NONE) i = (uint32_t)atomicAdd(&dsc->claim, 1ull);
+        if (w.sm->bcur[d] < w.sm->bend[d]) {
+          i = w.sm->bcur[d]++;
+        } else {
+          uint32_t old, k;
+          if (w.sm->pend[d] != PEND_NONE) {
+            old = w.sm->pend[d];
+            k = w.sm->pendk[d];
+            w.sm->pend[d] = PEND_NONE;
+          } else {
+            k = claim_batch(nP - min(nP, w.sm->bend[d]));
+            old = (uint32_t)atomicAdd(&dsc->claim, (unsigned long long)k);
+          }
+          i = old;
+          w.sm->bcur[d] = old + 1;
+          w.sm->bend[d] = min(old + k, nP);
+        }
       }
       i = __shfl_sync(FULLMASK, i, 0);
-      const uint32_t nP = w.sm->fnp[d];
       if (i >= nP) {
         // exhausted: wait for thieves still reading it, then pop
         if (lane == 0) {
@@ -1510,7 +1536,11 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         __syncwarp();
         continue;
       }
-      if (lane == 0) nxt = (i + 1 < nP) ? atomicAdd(&dsc->claim, 1ull) : (unsigned long long)nP;
+      if (lane == 0 && w.sm->bcur[d] >= w.sm->bend[d] && w.sm->bend[d] < nP) {
+        const uint32_t k2 = claim_batch(nP - w.sm->bend[d]);
+        nxt = atomicAdd(&dsc->claim, (unsigned long long)k2);
+        w.sm->pendk[d] = k2;
+      }
       F = w.arena + w.sm->foff[d];
       const uint32_t fsz = w.sm->fsz[d];
       if (fsz <= FC_WORDS) {
@@ -1587,7 +1617,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
     __syncwarp();
     if (lane == 0) {
       if (kind != 2) atomicAdd(&dsc->done, 1u);
-      if (kind == 1) w.sm->pend[d] = (uint32_t)nxt;
+      if (kind == 1 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
       if (kind == 3) w.steals++;
       if (p.flags & F_STATS) w.sm->ph[kind == 2 ? 0 : task_phase(F)] += clock64() - t0;
     }
