@@ -446,7 +446,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     return MBE_OK;
   }
   const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : 256;
-  const uint32_t ctas_per_sm = cfg.ctas_per_sm ? cfg.ctas_per_sm : 2;
+  // persistent kernel: every CTA must be co-resident, so clamp to the occupancy limit
+  const int max_res = mbe_search_max_ctas_per_sm((int)threads, mbe_search_smem_per_warp() * (int)(threads / 32));
+  if (max_res <= 0) return fail(MBE_ECUDA, "occupancy query failed for threads_per_cta=" + std::to_string(threads));
+  const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : 2u, (uint32_t)max_res);
   const uint32_t grid = (uint32_t)g->sm_count * ctas_per_sm;
   const uint32_t n_warps = grid * (threads / 32);
   // auto arena: proportional to the graph, 256 KiB .. 8 MiB per warp; grown x4 and retried on overflow

@@ -89,3 +89,4 @@ struct SearchParams {
 // ev0/ev1 (cudaEvent_t) bracket the search kernel alone.
 int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1);
 int mbe_search_smem_per_warp();
+int mbe_search_max_ctas_per_sm(int block, int smem_bytes);

@@ -218,7 +218,7 @@ __device__ __forceinline__ bool row_any_and(const Row<W>& a, const Row<W>& b) {
 
 // ------------------------------------------------------------------ sorting
 // Ascending sort of n (key, val) pairs in place (keys unique: (count << 32) | id).
-__device__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, int lane) {
+__device__ __noinline__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, int lane) {
   unsigned long long k = lane < (int)n ? key[lane] : ~0ull;
   uint32_t v = lane < (int)n ? val[lane] : 0u;
 #pragma unroll
@@ -352,7 +352,7 @@ __device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, 
 
 __device__ __forceinline__ uint32_t bit_length(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
 
-__device__ void sort_pairs_small(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
+__device__ __noinline__ void sort_pairs_small(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
   if (n <= 1) return;
   if (n <= 32) sort_regs32(key, val, n, lane);
   else sort_smem(key, val, n, sm, lane);
@@ -602,11 +602,11 @@ __device__ __forceinline__ void account_emit(Warp& w, const SearchParams& p, uin
 
 // Bounded listing: record (A, B) in original ids.  Lids: L' (V ids) sorted;
 // R' = Rfr (frame R, U ranks) ∪ {x} ∪ rexp (U ranks).
-__device__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lids, uint32_t nL, const uint32_t* Rfr,
+__device__ __noinline__ void write_record(const int lane, const SearchParams& p, const uint32_t* Lids, uint32_t nL, const uint32_t* Rfr,
                              uint32_t nRf, uint32_t x, const uint32_t* rexp, uint32_t nRx) {
   uint32_t nR = nRf + 1 + nRx;
   unsigned long long rec = 0, ido = 0;
-  if (w.lane == 0) {
+  if (lane == 0) {
     rec = atomicAdd(&p.gl->out_records, 1ull);
     ido = atomicAdd(&p.gl->out_ids, (unsigned long long)(nL + nR));
   }
@@ -614,7 +614,7 @@ __device__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lid
   ido = __shfl_sync(FULLMASK, ido, 0);
   if (rec >= p.cap_records) return;
   if (ido + nL + nR > p.cap_ids) {
-    if (w.lane == 0) p.rec_off[rec] = ~0ull;  // record counted but its ids did not fit
+    if (lane == 0) p.rec_off[rec] = ~0ull;  // record counted but its ids did not fit
     return;
   }
   uint32_t nA = p.cand_side == 1 ? nR : nL;
@@ -622,12 +622,12 @@ __device__ void write_record(Warp& w, const SearchParams& p, const uint32_t* Lid
   uint32_t offR = p.cand_side == 1 ? 0u : nL;
   uint32_t offL = p.cand_side == 1 ? nR : 0u;
   unsigned int* ids = p.out_ids + ido;
-  for (uint32_t t = w.lane; t < nL; t += 32) ids[offL + t] = Lids[t];
-  for (uint32_t t = w.lane; t < nR; t += 32) {
+  for (uint32_t t = lane; t < nL; t += 32) ids[offL + t] = Lids[t];
+  for (uint32_t t = lane; t < nR; t += 32) {
     uint32_t r = t < nRf ? Rfr[t] : (t == nRf ? x : rexp[t - nRf - 1]);
     ids[offR + t] = p.g.origU[r];
   }
-  if (w.lane == 0) {
+  if (lane == 0) {
     p.rec_off[rec] = ido;
     p.rec_n1[rec] = nA;
     p.rec_n2[rec] = nB;
@@ -906,7 +906,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   const uint32_t nRp = nR + 1 + nRx;
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, nLp, sRp, nRp);
-  if (p.cap_records) write_record(w, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
+  if (p.cap_records) write_record(w.lane, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
   if (nPc == 0) return;
 
   // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.  A wide (8/16-word)
@@ -1077,7 +1077,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     if (bit) lbuf[before + __popc(b & lanemask_lt())] = L[q * 32 + lane];
   }
   __syncwarp();
-  if (p.cap_records) write_record(w, p, lbuf, k, R, nR, x, rbuf, nRx);
+  if (p.cap_records) write_record(w.lane, p, lbuf, k, R, nR, x, rbuf, nRx);
   if (!need_child) return;
 
   // Q' candidates: frame Q rows and Q-role siblings P[j<i] meeting L'
@@ -1256,7 +1256,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   const uint32_t nRp = nR + 1 + nRx;
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, k, sRp, nRp);
-  if (p.cap_records) write_record(w, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
+  if (p.cap_records) write_record(w.lane, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
   MBE_PHASE(12, tph);
   if (nPc == 0) return;
 
@@ -1706,6 +1706,15 @@ __global__ void __launch_bounds__(256) mbe_twin_kernel(DevGraph g, uint8_t* twin
 }  // namespace
 
 int mbe_search_smem_per_warp() { return (int)sizeof(WarpSmem); }
+
+// Resident CTAs per SM for a launch shape (the persistent kernel needs every CTA co-resident).
+int mbe_search_max_ctas_per_sm(int block, int smem_bytes) {
+  if (cudaFuncSetAttribute(mbe_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+    return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mbe_search_kernel, block, smem_bytes) != cudaSuccess) return 0;
+  return n;
+}
 
 int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
