@@ -63,6 +63,7 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t *row_ptr, const uint32
 #define MBE_STATS 0x2u        /* count algorithmic bytes / task kinds (small overhead) */
 #define MBE_NO_ANTICHAIN 0x4u /* keep every Q' row instead of the antichain (result-invariant, slower) */
 #define MBE_NO_TWIN 0x8u      /* disable root-level twin pre-pruning (result-invariant) */
+#define MBE_STEAL_ONE 0x10u   /* thieves take one task at a time instead of half a frame (result-invariant) */
 
 typedef struct {
   uint32_t struct_size;      /* ABI versioning: sizeof(mbe_config) */

@@ -30,9 +30,12 @@ struct DevGraph {
 
 // Published frame descriptor (one per warp per depth).  claim = (nP << 32) | next.
 struct Desc {
-  unsigned long long claim;
-  unsigned int done;
-  unsigned int off;  // word offset of the frame in the owner's arena
+  unsigned long long claim;  // (task limit << 32) | next unclaimed task
+  unsigned int done;         // tasks finished (or handed to a thief's copy) since publication
+  unsigned int off;          // word offset of the frame in the owner's arena
+  unsigned int size;         // frame size in words
+  unsigned int first;        // first task index of this frame's range (copies made by thieves)
+  unsigned int pad[2];
 };
 
 struct Globals {
@@ -84,6 +87,7 @@ struct SearchParams {
 #define F_STATS 0x2u
 #define F_NO_ANTICHAIN 0x4u
 #define F_NO_TWIN 0x8u
+#define F_STEAL_ONE 0x10u
 
 // Launches the twin pre-pass and the persistent search kernel on `stream`;
 // ev0/ev1 (cudaEvent_t) bracket the search kernel alone.

@@ -45,7 +45,8 @@ struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligne
   unsigned int sval[MBE_SMEM_SORT];
   unsigned int hist[256];
   unsigned int foff[MBE_MAXDEPTH];  // arena word offset of the frame at each depth
-  unsigned int fnp[MBE_MAXDEPTH];   // its |P| (task count)
+  unsigned int fnp[MBE_MAXDEPTH];   // its task limit (|P|, or the end of a stolen range)
+  unsigned int ffirst[MBE_MAXDEPTH];  // first task of its range (0 unless a thief's copy)
   unsigned int pend[MBE_MAXDEPTH];  // prefetched claim result (PEND_NONE = none)
   unsigned int pendk[MBE_MAXDEPTH]; // size of the prefetched claim
   unsigned int bcur[MBE_MAXDEPTH];  // owner's claimed batch [bcur, bend) at each depth
@@ -646,23 +647,27 @@ __device__ __forceinline__ bool arena_reserve(Warp& w, const SearchParams& p, ui
 }
 
 // Publish the frame just written at arena offset w.atop (size words) as depth w.top.
-__device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_words, uint32_t nP) {
+__device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_words, uint32_t nP,
+                              uint32_t first = 0u) {
   __syncwarp();
   if (w.lane == 0) {
     Desc* d = &w.desc[w.top];
     d->off = (unsigned int)w.atop;
     d->done = 0u;
+    d->size = (unsigned int)size_words;
+    d->first = first;
     w.sm->foff[w.top] = (unsigned int)w.atop;
     w.sm->fnp[w.top] = nP;
+    w.sm->ffirst[w.top] = first;
     w.sm->pend[w.top] = PEND_NONE;
     w.sm->bcur[w.top] = 0u;
     w.sm->bend[w.top] = 0u;
     w.sm->fsz[w.top] = (unsigned int)size_words;
     if (w.sm->fc_depth == (int)w.top) w.sm->fc_depth = -1;
     __threadfence();
-    atomicExch(&d->claim, ((unsigned long long)nP) << 32);
+    atomicExch(&d->claim, (((unsigned long long)nP) << 32) | first);
     p.tops[w.gw] = w.top + 1;
-    if (nP >= 2 && !(p.flags & F_NO_STEAL)) atomicOr(&p.hint[w.gw >> 5], 1u << (w.gw & 31));
+    if (nP - first >= 2 && !(p.flags & F_NO_STEAL)) atomicOr(&p.hint[w.gw >> 5], 1u << (w.gw & 31));
     w.frames++;
   }
   w.atop = align4(w.atop + size_words);
@@ -1364,7 +1369,8 @@ __device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p)
 // and claim ONE task of the bottom-most such frame (largest subtree).
 // Returns true with (*victim, *depth, *task) on success.
 __device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const SearchParams& p, uint32_t rot,
-                                       uint32_t* victim, uint32_t* depth, uint32_t* task) {
+                                       bool steal_half, uint32_t* victim, uint32_t* depth, uint32_t* task,
+                                       uint32_t* task_end) {
   const uint32_t nw = (p.n_warps + 31) >> 5;
   const uint32_t start = ((gw + 1 + rot) % p.n_warps) >> 5;
   int probes = 0;
@@ -1399,18 +1405,26 @@ __device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const 
           }
           if (found >= 0) {
             // leave the idle set before claiming, so termination cannot be declared while this
-            // warp holds a claimed task; re-enter it if the claim is lost
+            // warp holds claimed tasks; re-enter it if the claim is lost.  Claim about half of
+            // the unclaimed tasks (the range is copied into this warp's own frame).
             unsigned long long old = 0;
+            uint32_t k = 1;
             if (lane == 0) {
+              unsigned long long* cw = &p.desc[(size_t)v * MBE_MAXDEPTH + found].claim;
+              const unsigned long long c = ld_volatile64(cw);
+              const uint32_t rem = (uint32_t)(c >> 32) > (uint32_t)c ? (uint32_t)(c >> 32) - (uint32_t)c : 1u;
+              k = steal_half ? max(1u, rem / 2) : 1u;
               atomicSub(&p.gl->idle, 1u);
-              old = atomicAdd(&p.desc[(size_t)v * MBE_MAXDEPTH + found].claim, 1ull);
+              old = atomicAdd(cw, (unsigned long long)k);
               if ((uint32_t)old >= (uint32_t)(old >> 32)) atomicAdd(&p.gl->idle, 1u);
             }
             old = __shfl_sync(FULLMASK, old, 0);
+            k = __shfl_sync(FULLMASK, k, 0);
             if ((uint32_t)old < (uint32_t)(old >> 32)) {
               *victim = v;
               *depth = (uint32_t)found;
               *task = (uint32_t)old;
+              *task_end = min((uint32_t)old + k, (uint32_t)(old >> 32));
               return true;
             }
           }
@@ -1516,7 +1530,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       if (i >= nP) {
         // exhausted: wait for thieves still reading it, then pop
         if (lane == 0) {
-          while (ld_volatile(&dsc->done) < nP) {
+          while (ld_volatile(&dsc->done) < nP - w.sm->ffirst[d]) {
             if (ld_volatile(&p.gl->error) || globaltimer_ns() - t_start > p.watchdog_ns) {
               set_error(p, 4u, 1ull);
               w.failed = true;
@@ -1584,10 +1598,11 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         }
       }
       if (__shfl_sync(FULLMASK, stop, 0)) break;
-      uint32_t v = 0, vdep = 0;
+      uint32_t v = 0, vdep = 0, tend = 0;
       bool got = false;
       if (steal) {
-        got = try_steal(lane, gw, p, rot, &v, &vdep, &ti);  // leaves the idle set only on a successful claim
+        // leaves the idle set only on a successful claim
+        got = try_steal(lane, gw, p, rot, !(p.flags & F_STEAL_ONE), &v, &vdep, &ti, &tend);
         rot += 97;
       }
       if (!got) {
@@ -1604,6 +1619,23 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       dsc = p.desc + (size_t)v * MBE_MAXDEPTH + vdep;
       const uint32_t off = ld_volatile(&dsc->off);
       F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)v * p.ws_stride + p.o_arena) + off;
+      if (tend - ti >= 2) {
+        // steal-half: copy the victim's frame into this warp's (empty) arena and publish it as
+        // this warp's own frame over the claimed range [ti, tend); then release the victim
+        const uint32_t fsz = ld_volatile(&dsc->size);
+        if (!arena_reserve(w, p, fsz + 8)) break;
+        const uint4* src = reinterpret_cast<const uint4*>(F);
+        uint4* dst = reinterpret_cast<uint4*>(w.arena + w.atop);
+        for (uint32_t t = lane; t < (fsz + 3) / 4; t += 32) dst[t] = src[t];
+        __syncwarp();
+        if (lane == 0) {
+          atomicAdd(&dsc->done, tend - ti);  // the victim no longer needs to wait for this range
+          w.steals += tend - ti;
+          if (p.flags & F_STATS) w.sm->ph[3] += clock64() - t0;
+        }
+        publish_frame(w, p, fsz, tend, ti);
+        continue;
+      }
       if (lane == 0 && (p.flags & F_STATS)) {
         const unsigned long long now = clock64();
         w.sm->ph[3] += now - t0;
