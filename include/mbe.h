@@ -118,6 +118,8 @@ typedef struct {
    * Sub-phases of bit-row tasks: [11] maximality check, [12] expansion + emit, [13] Q' rows +
    * ordering, [14] child frame build.  [15] reserved. */
   uint64_t phase_cycles[16];
+  uint64_t max_task_cycles[3]; /* MBE_STATS: longest single task in cycles: [0] level-1, [1] list, [2] bit-row */
+  double roots_out_ms;         /* MBE_STATS: time after launch when the level-1 subtree list ran out */
 } mbe_result;
 
 /* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be

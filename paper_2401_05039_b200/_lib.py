@@ -44,7 +44,8 @@ class mbe_result(ctypes.Structure):
     _fields_ = [("count", _u64), ("hash", _u64), ("tasks", _u64), ("pruned", _u64), ("steals", _u64),
                 ("records_written", _u64), ("truncated", _u32), ("candidate_side", _i32), ("kernel_ms", _dbl),
                 ("wall_ms", _dbl), ("alg_bytes", _u64), ("list_tasks", _u64), ("bitmap_tasks", _u64),
-                ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 16)]
+                ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 16),
+                ("max_task_cycles", _u64 * 3), ("roots_out_ms", _dbl)]
 
 
 class mbe_graph_info(ctypes.Structure):
@@ -113,6 +114,8 @@ class Result:
     records_written: int = 0
     truncated: bool = False
     phase_cycles: tuple = ()
+    max_task_cycles: tuple = ()
+    roots_out_ms: float = -1.0
 
 
 def mbe_strerror(code: int) -> str:
@@ -168,7 +171,8 @@ def mbe_enumerate(handle: int, config: Optional[mbe_config] = None, output: Opti
                   int(res.candidate_side), float(res.kernel_ms), float(res.wall_ms), int(res.alg_bytes),
                   int(res.list_tasks), int(res.bitmap_tasks), int(res.frames), int(res.n_warps),
                   int(res.max_depth), int(res.records_written), bool(res.truncated),
-                  tuple(int(v) for v in res.phase_cycles))
+                  tuple(int(v) for v in res.phase_cycles), tuple(int(v) for v in res.max_task_cycles),
+                  float(res.roots_out_ms))
 
 
 def mbe_get_info(handle: int) -> dict:

@@ -572,6 +572,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.out_ids = (unsigned int*)lb.ids.p;
 
     CUDA_TRY(cudaMemsetAsync(W->gl.p, 0, sizeof(Globals), st));
+    CUDA_TRY(cudaMemsetAsync(&static_cast<Globals*>(W->gl.p)->t_roots_out, 0xff, 8, st));
     CUDA_TRY(cudaMemsetAsync(W->desc.p, 0, sizeof(Desc) * MBE_MAXDEPTH * n_warps, st));
     CUDA_TRY(cudaMemsetAsync(W->tops.p, 0, 4ull * n_warps, st));
     CUDA_TRY(cudaMemsetAsync(W->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
@@ -609,6 +610,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     res->n_warps = n_warps;
     res->max_depth = hg.max_depth;
     for (int k = 0; k < 16; ++k) res->phase_cycles[k] = hg.phase[k];
+    for (int k = 0; k < 3; ++k) res->max_task_cycles[k] = hg.max_task[k];
+    res->roots_out_ms = hg.t_roots_out == ~0ull ? -1.0 : (double)hg.t_roots_out * 1e-6;
     if (cfg.per_root) {
       std::vector<uint64_t> pr(4ull * S.nU);
       CUDA_TRY(cudaMemcpy(pr.data(), W->per_root.p, 32ull * S.nU, cudaMemcpyDeviceToHost));

@@ -1579,6 +1579,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       pos = __shfl_sync(FULLMASK, pos, 0);
       if (pos >= p.g.n_roots) {
         roots_done = true;
+        if (lane == 0 && (p.flags & F_STATS)) atomicMin(&p.gl->t_roots_out, globaltimer_ns() - t_start);
         continue;
       }
       xr = p.g.root_order[pos];
@@ -1651,7 +1652,12 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       if (kind != 2) atomicAdd(&dsc->done, 1u);
       if (kind == 1 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
       if (kind == 3) w.steals++;
-      if (p.flags & F_STATS) w.sm->ph[kind == 2 ? 0 : task_phase(F)] += clock64() - t0;
+      if (p.flags & F_STATS) {
+        const int ph = kind == 2 ? 0 : task_phase(F);
+        const unsigned long long dt = clock64() - t0;
+        w.sm->ph[ph] += dt;
+        atomicMax(&p.gl->max_task[ph], dt);
+      }
     }
     __syncwarp();
   }
