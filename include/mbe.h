@@ -120,6 +120,7 @@ typedef struct {
   uint64_t phase_cycles[16];
   uint64_t max_task_cycles[3]; /* MBE_STATS: longest single task in cycles: [0] level-1, [1] list, [2] bit-row */
   double roots_out_ms;         /* MBE_STATS: time after launch when the level-1 subtree list ran out */
+  uint64_t max_phase_cycles[16]; /* MBE_STATS: longest single occurrence of each phase_cycles sub-phase */
 } mbe_result;
 
 /* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be

@@ -45,7 +45,7 @@ class mbe_result(ctypes.Structure):
                 ("records_written", _u64), ("truncated", _u32), ("candidate_side", _i32), ("kernel_ms", _dbl),
                 ("wall_ms", _dbl), ("alg_bytes", _u64), ("list_tasks", _u64), ("bitmap_tasks", _u64),
                 ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 16),
-                ("max_task_cycles", _u64 * 3), ("roots_out_ms", _dbl)]
+                ("max_task_cycles", _u64 * 3), ("roots_out_ms", _dbl), ("max_phase_cycles", _u64 * 16)]
 
 
 class mbe_graph_info(ctypes.Structure):
@@ -116,6 +116,7 @@ class Result:
     phase_cycles: tuple = ()
     max_task_cycles: tuple = ()
     roots_out_ms: float = -1.0
+    max_phase_cycles: tuple = ()
 
 
 def mbe_strerror(code: int) -> str:
@@ -172,7 +173,7 @@ def mbe_enumerate(handle: int, config: Optional[mbe_config] = None, output: Opti
                   int(res.list_tasks), int(res.bitmap_tasks), int(res.frames), int(res.n_warps),
                   int(res.max_depth), int(res.records_written), bool(res.truncated),
                   tuple(int(v) for v in res.phase_cycles), tuple(int(v) for v in res.max_task_cycles),
-                  float(res.roots_out_ms))
+                  float(res.roots_out_ms), tuple(int(v) for v in res.max_phase_cycles))
 
 
 def mbe_get_info(handle: int) -> dict:

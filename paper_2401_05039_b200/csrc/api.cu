@@ -611,6 +611,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     res->max_depth = hg.max_depth;
     for (int k = 0; k < 16; ++k) res->phase_cycles[k] = hg.phase[k];
     for (int k = 0; k < 3; ++k) res->max_task_cycles[k] = hg.max_task[k];
+    for (int k = 0; k < 16; ++k) res->max_phase_cycles[k] = hg.max_phase[k];
     res->roots_out_ms = hg.t_roots_out == ~0ull ? -1.0 : (double)hg.t_roots_out * 1e-6;
     if (cfg.per_root) {
       std::vector<uint64_t> pr(4ull * S.nU);

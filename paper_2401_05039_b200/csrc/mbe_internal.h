@@ -51,6 +51,7 @@ struct Globals {
   unsigned long long phase[16];  // MBE_STATS: Σ over warps of cycles per phase (see mbe.h)
   unsigned long long max_task[4];  // MBE_STATS: longest single task (cycles): root, list, bit-row, -
   unsigned long long t_roots_out;  // MBE_STATS: ns after launch when the level-1 list ran out
+  unsigned long long max_phase[16];  // MBE_STATS: longest single occurrence of each sub-phase (cycles)
 };
 
 struct SearchParams {

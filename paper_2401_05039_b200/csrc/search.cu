@@ -125,6 +125,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     if ((p.flags & F_STATS) && w.lane == 0) {                        \
       unsigned long long now_ = (unsigned long long)clock64();       \
       w.sm->ph[k] += now_ - (t);                                     \
+      atomicMax(&p.gl->max_phase[k], now_ - (t));                    \
       (t) = now_;                                                    \
     }                                                                \
   } while (0)

@@ -47,6 +47,7 @@ def main():
                                                        for c in st.phase_cycles[:15]],
                               max_task_ms=[round(c / 1.965e6, 3) for c in st.max_task_cycles],
                               roots_out_ms=round(st.roots_out_ms, 3),
+                              max_phase_ms=[round(c / 1.965e6, 3) for c in st.max_phase_cycles[:15]],
                               bicliques_per_s=r.count / (min(times) / 1e3))), flush=True)
         G.close()
 
