@@ -432,6 +432,54 @@ __device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint
   return K;
 }
 
+// Exact-duplicate removal before the antichain for large candidate sets: sort
+// the rows by (popcount descending, 32-bit row hash) with the warp radix sort,
+// then keep a row unless it equals its predecessor.  Output rows are in
+// descending popcount order.  (Equal rows get equal keys; distinct rows that
+// collide on the hash are compared word by word, so the result is exact.)
+__device__ __noinline__ uint32_t dedup_sort_rows(const uint32_t* src, uint32_t n, uint32_t W, uint32_t* dst,
+                                                 unsigned long long* key, uint32_t* val, unsigned long long* key2,
+                                                 uint32_t* val2, WarpSmem* sm, int lane) {
+  for (uint32_t t = lane; t < n; t += 32) {
+    const uint32_t* r = src + (size_t)t * W;
+    uint32_t pc = 0, h = 0x9E3779B9u;
+    for (uint32_t q = 0; q < W; ++q) {
+      const uint32_t a = r[q];
+      pc += __popc(a);
+      h = (h ^ a) * 0x01000193u;
+      h ^= h >> 15;
+    }
+    key[t] = ((unsigned long long)(W * 32u - pc) << 32) | h;
+    val[t] = t;
+  }
+  __syncwarp();
+  sort_radix(key, val, key2, val2, n, 32, bit_length(W * 32u), sm, lane);
+  uint32_t m = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t t = base + lane;
+    bool keep = false;
+    if (t < n) {
+      keep = true;
+      if (t > 0 && key[t] == key[t - 1]) {
+        const uint32_t* a = src + (size_t)val[t] * W;
+        const uint32_t* b = src + (size_t)val[t - 1] * W;
+        uint32_t x = 0;
+        for (uint32_t q = 0; q < W; ++q) x |= a[q] ^ b[q];
+        keep = x != 0u;
+      }
+    }
+    const uint32_t bk = __ballot_sync(FULLMASK, keep);
+    if (keep) {
+      const uint32_t* a = src + (size_t)val[t] * W;
+      uint32_t* o = dst + (size_t)(m + __popc(bk & lanemask_lt())) * W;
+      for (uint32_t q = 0; q < W; ++q) o[q] = a[q];
+    }
+    m += __popc(bk);
+  }
+  __syncwarp();
+  return m;
+}
+
 // Same reduction for wide rows (8 or 16 words), word-sliced: rows are streamed from
 // memory (L1) instead of held in registers.
 __device__ __forceinline__ bool wide_subset(const uint32_t* a, const uint32_t* b, uint32_t W) {  // a ⊆ b
@@ -942,7 +990,14 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     }
     uint32_t* CQ = CPr + (size_t)nPc * Wc;
     __syncwarp();
-    nQk = antichain_w(Wc, w.qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+    const uint32_t* qsrc = w.qbuf;
+    uint32_t qn = nQc;
+    if (!(p.flags & F_NO_ANTICHAIN) && nQc > 96) {  // large Q': drop exact duplicates first
+      qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
+                           w.sm, lane);
+      qsrc = w.pbuf;
+    }
+    nQk = antichain_w(Wc, qsrc, qn, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
     size = (uint64_t)(CQ + (size_t)nQk * Wc - C);
   } else {
     uint32_t* CK = CP + nPc;
