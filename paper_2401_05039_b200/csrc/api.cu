@@ -534,6 +534,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       p.wide_qcap = q ? (uint32_t)std::strtoul(q, nullptr, 10) : 256u;
       const char* r = std::getenv("MBE_WIDE_RATIO");
       p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 16u;
+      const char* dm = std::getenv("MBE_DEDUP_MIN");
+      p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 2048u;
     }
     p.flags = cfg.flags;
     p.rank = cfg.rank;
