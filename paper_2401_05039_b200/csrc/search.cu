@@ -992,7 +992,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     __syncwarp();
     const uint32_t* qsrc = w.qbuf;
     uint32_t qn = nQc;
-    if (!(p.flags & F_NO_ANTICHAIN) && nQc > p.dedup_min) {  // large Q': drop exact duplicates first
+    if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
       qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
                            w.sm, lane);
       qsrc = w.pbuf;
