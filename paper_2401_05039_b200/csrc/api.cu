@@ -533,7 +533,9 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       const char* q = std::getenv("MBE_WIDE_QCAP");
       p.wide_qcap = q ? (uint32_t)std::strtoul(q, nullptr, 10) : 256u;
       const char* r = std::getenv("MBE_WIDE_RATIO");
-      p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 16u;
+      p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 64u;
+      const char* qm = std::getenv("MBE_WIDE_QMAX");
+      p.wide_qmax = qm ? (uint32_t)std::strtoul(qm, nullptr, 10) : 4096u;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
       p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 8192u;
     }

@@ -59,7 +59,8 @@ struct SearchParams {
   int cand_side;  // 1 or 2 (A/B orientation of the hash)
   uint32_t T;     // bitmap threshold (<= 32 * MBE_WMAX = 512)
   uint32_t wide_qcap;   // relocalize a list task's child into 8/16-word rows if |Q'| <= wide_qcap
-  uint32_t wide_ratio;  //   ... or |Q'| <= wide_ratio * |P'|
+  uint32_t wide_ratio;  //   ... or |Q'| <= wide_ratio * |P'| and |Q'| <= wide_qmax
+  uint32_t wide_qmax;
   uint32_t dedup_min;   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;
   uint32_t rank, world;
