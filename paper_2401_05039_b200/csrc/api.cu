@@ -535,7 +535,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       const char* r = std::getenv("MBE_WIDE_RATIO");
       p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 64u;
       const char* qm = std::getenv("MBE_WIDE_QMAX");
-      p.wide_qmax = qm ? (uint32_t)std::strtoul(qm, nullptr, 10) : 4096u;
+      p.wide_qmax = qm ? (uint32_t)std::strtoul(qm, nullptr, 10) : 0xffffffffu;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
       p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 8192u;
     }

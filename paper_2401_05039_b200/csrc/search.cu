@@ -449,11 +449,11 @@ __device__ __noinline__ uint32_t dedup_sort_rows(const uint32_t* src, uint32_t n
       h = (h ^ a) * 0x01000193u;
       h ^= h >> 15;
     }
-    key[t] = ((unsigned long long)(W * 32u - pc) << 32) | h;
+    key[t] = ((unsigned long long)(W * 32u - pc) << 32) | (h & 0xffffffu);
     val[t] = t;
   }
   __syncwarp();
-  sort_radix(key, val, key2, val2, n, 32, bit_length(W * 32u), sm, lane);
+  sort_radix(key, val, key2, val2, n, 24, bit_length(W * 32u), sm, lane);
   uint32_t m = 0;
   for (uint32_t base = 0; base < n; base += 32) {
     const uint32_t t = base + lane;
@@ -510,7 +510,8 @@ __device__ __forceinline__ bool meta_may_subset(unsigned long long a, unsigned l
 }
 
 __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* dst, uint32_t W, bool keep_all,
-                                   int lane, unsigned long long* kmeta /* smem [MBE_SMEM_SORT] */) {
+                                   int lane, unsigned long long* kmeta /* smem [MBE_SMEM_SORT] */,
+                                   unsigned long long* kmeta_g /* global spill for kept rows >= MBE_SMEM_SORT, or null */) {
   if (keep_all) {
     for (uint32_t t = lane; t < n * W; t += 32) dst[t] = src[t];
     __syncwarp();
@@ -524,7 +525,8 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
     const unsigned long long mr = valid ? wide_meta(r, W) : 0ull;
     bool dom = !valid;
     for (uint32_t k = 0; k < K; ++k) {
-      const unsigned long long mk = k < MBE_SMEM_SORT ? kmeta[k] : wide_meta(dst + (size_t)k * W, W);
+      const unsigned long long mk =
+          k < MBE_SMEM_SORT ? kmeta[k] : (kmeta_g ? kmeta_g[k] : wide_meta(dst + (size_t)k * W, W));
       if (!dom && meta_may_subset(mr, mk) && wide_subset(r, dst + (size_t)k * W, W)) dom = true;
     }
     const uint32_t vb = __ballot_sync(FULLMASK, valid);
@@ -543,7 +545,8 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
         const bool kval = kb + lane < K;
         const uint32_t kk = kval ? kb + lane : 0u;
         const uint32_t* kr = dst + (size_t)kk * W;
-        const unsigned long long mk = kval ? (kk < MBE_SMEM_SORT ? kmeta[kk] : wide_meta(kr, W)) : 0ull;
+        const unsigned long long mk =
+            kval ? (kk < MBE_SMEM_SORT ? kmeta[kk] : (kmeta_g ? kmeta_g[kk] : wide_meta(kr, W))) : 0ull;
         bool kdom = false;
         for (int m = 0; m < 32; ++m) {
           const unsigned long long ms = __shfl_sync(FULLMASK, mr, m);
@@ -561,6 +564,7 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
           uint32_t* o = dst + (size_t)ni * W;
           for (uint32_t q = 0; q < W; ++q) o[q] = row[q];
           if (ni < MBE_SMEM_SORT) kmeta[ni] = mk;
+          else if (kmeta_g) kmeta_g[ni] = mk;
         }
         newK += __popc(bk);
         __syncwarp();
@@ -571,6 +575,7 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
         uint32_t* o = dst + (size_t)ni * W;
         for (uint32_t q = 0; q < W; ++q) o[q] = r[q];
         if (ni < MBE_SMEM_SORT) kmeta[ni] = mr;
+        else if (kmeta_g) kmeta_g[ni] = mr;
       }
       K += __popc(bs);
       __syncwarp();
@@ -580,11 +585,12 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
 }
 
 __device__ __forceinline__ uint32_t antichain_w(uint32_t Wc, const uint32_t* src, uint32_t n, uint32_t* dst,
-                                                bool keep_all, int lane, WarpSmem* sm) {
+                                                bool keep_all, int lane, WarpSmem* sm,
+                                                unsigned long long* kmeta_g = nullptr) {
   if (Wc == 1) return antichain<1>(src, n, dst, keep_all, lane);
   if (Wc == 2) return antichain<2>(src, n, dst, keep_all, lane);
   if (Wc == 4) return antichain<4>(src, n, dst, keep_all, lane);
-  return antichain_wide(src, n, dst, Wc, keep_all, lane, sm->skey);
+  return antichain_wide(src, n, dst, Wc, keep_all, lane, sm->skey, kmeta_g);
 }
 
 // ------------------------------------------------------------------ misc
@@ -997,7 +1003,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
                            w.sm, lane);
       qsrc = w.pbuf;
     }
-    nQk = antichain_w(Wc, qsrc, qn, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+    nQk = antichain_w(Wc, qsrc, qn, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm, w.skey);
     size = (uint64_t)(CQ + (size_t)nQk * Wc - C);
   } else {
     uint32_t* CK = CP + nPc;
