@@ -1417,6 +1417,29 @@ __device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const u
   }
 }
 
+// Maximality check of task i on a 1-word bit-row frame (Step 3): an identical
+// earlier sibling (R2, equal-key block) or a Q row containing row(x) prunes it.
+__device__ __forceinline__ bool w1_pruned(const uint32_t* F, uint32_t i, int lane) {
+  const uint32_t nL = F[1], nP = F[2], nQ = F[3], nR = F[4];
+  const uint32_t* Prow = F + align4((uint64_t)MBE_HDR_WORDS + nL + nR + nP);
+  const uint32_t* Qrow = Prow + nP;
+  const uint32_t lx = Prow[i];
+  const uint32_t k = __popc(lx);
+  for (uint32_t cb = 0; cb < i; cb += 32) {
+    const int j = (int)i - 1 - (int)cb - lane;
+    const bool valid = j >= 0;
+    const uint32_t r = valid ? Prow[j] : 0u;
+    if (__any_sync(FULLMASK, valid && r == lx)) return true;
+    if (__any_sync(FULLMASK, !valid || (uint32_t)__popc(r) < k)) break;
+  }
+  for (uint32_t qb = 0; qb < nQ; qb += 32) {
+    const bool valid = qb + lane < nQ;
+    const uint32_t r = valid ? Qrow[qb + lane] : 0u;
+    if (__any_sync(FULLMASK, valid && (lx & ~r) == 0u)) return true;
+  }
+  return false;
+}
+
 // Owner batch size from the number of tasks not yet claimed by it (an upper bound).
 __device__ __forceinline__ uint32_t claim_batch(uint32_t rem) {
   return rem >= 64u ? 8u : (rem >= 16u ? 4u : (rem >= 6u ? 2u : 1u));
@@ -1631,6 +1654,31 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       }
       ti = i;
       kind = 1;
+      // Fast path: most tasks are 1-word bit-row tasks pruned by the maximality check (SURVEY
+      // fact 8); decide those here with a few shared-memory reads, outside the general task
+      // code, so the hot instruction stream stays small.
+      if (F == w.sm->fcache && F[0] == (KIND_BITMAP | (1u << 8)) && w1_pruned(F, i, lane)) {
+        if (lane == 0) {
+          w.tasks++;
+          w.pruned++;
+          if (p.per_root) {
+            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 2], 1ull);
+            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 3], 1ull);
+          }
+          atomicAdd(&dsc->done, 1u);
+          if (nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
+          if (p.flags & F_STATS) {
+            w.bitmap_tasks++;
+            const uint32_t nP_ = F[2], nQ_ = F[3];
+            w.alg_bytes += 4ull * (1ull + nP_ + nQ_) + 4ull * nP_;
+            const unsigned long long dt = clock64() - t0;
+            w.sm->ph[2] += dt;
+            w.sm->ph[11] += dt;
+          }
+        }
+        __syncwarp();
+        continue;
+      }
     } else if (!roots_done) {
       // ---- empty stack: next level-1 subtree (coarse-grained task)
       unsigned long long pos = 0;
