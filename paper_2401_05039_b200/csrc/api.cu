@@ -536,6 +536,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 64u;
       const char* qm = std::getenv("MBE_WIDE_QMAX");
       p.wide_qmax = qm ? (uint32_t)std::strtoul(qm, nullptr, 10) : 0xffffffffu;
+      const char* nq = std::getenv("MBE_NARROW_QMAX");
+      p.narrow_qmax = nq ? (uint32_t)std::strtoul(nq, nullptr, 10) : 0u;
+      const char* nr = std::getenv("MBE_NARROW_RATIO");
+      p.narrow_ratio = nr ? (uint32_t)std::strtoul(nr, nullptr, 10) : 256u;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
       p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 8192u;
     }

@@ -61,6 +61,7 @@ struct SearchParams {
   uint32_t wide_qcap;   // relocalize a list task's child into 8/16-word rows if |Q'| <= wide_qcap
   uint32_t wide_ratio;  //   ... or |Q'| <= wide_ratio * |P'| and |Q'| <= wide_qmax
   uint32_t wide_qmax;
+  uint32_t narrow_qmax, narrow_ratio;  // same guard for 1/2/4-word children (narrow_qmax 0 = always)
   uint32_t dedup_min;   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;
   uint32_t rank, world;

@@ -973,7 +973,8 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   // bit-row child is built only when its Q' is small (p.wide_qcap) or small relative to the
   // number of sibling tasks that will reuse it (p.wide_ratio), since one warp builds it serially;
   // otherwise the child stays a list frame (implicit Q is exact either way).
-  const bool cbm = bm && (Wc <= 4 || nQc <= p.wide_qcap || (nQc <= p.wide_ratio * nPc && nQc <= p.wide_qmax));
+  const bool cbm = bm && (Wc <= 4 ? (p.narrow_qmax == 0 || nQc <= p.narrow_qmax || nQc <= p.narrow_ratio * nPc)
+                                  : (nQc <= p.wide_qcap || (nQc <= p.wide_ratio * nPc && nQc <= p.wide_qmax)));
   warp_sort_pairs(w, p, nPc, nLp);
   MBE_PHASE(9, tph);
   const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
