@@ -765,6 +765,8 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   }
 
   unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+  const unsigned long long tstart = tph;
+  unsigned long long tsub[5] = {0, 0, 0, 0, 0};
   // Step 2: L' = L ∩ N(x)
   const uint32_t* Lp;
   uint32_t nLp;
@@ -795,6 +797,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     __syncwarp();
   }
 
+  if ((p.flags & F_STATS) && lane == 0) tsub[0] = (unsigned long long)clock64() - tph;
   MBE_PHASE(6, tph);
   // Reverse scan: for u ∈ L' (position pos), for v ∈ N(u): cnt[v]++,
   // bit pos of row(v) when building a bit-row child.  Flattened over the warp.
@@ -861,6 +864,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   sL = warp_sum64(sL);
   __syncwarp();
 
+  if ((p.flags & F_STATS) && lane == 0) tsub[1] = (unsigned long long)clock64() - tph;
   MBE_PHASE(7, tph);
   // Classification of every touched vertex (Steps 3 and 4).
   bool nonmax = false;
@@ -954,6 +958,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   sRx = warp_sum64(sRx);
   __syncwarp();
 
+  if ((p.flags & F_STATS) && lane == 0) tsub[2] = (unsigned long long)clock64() - tph;
   MBE_PHASE(8, tph);
   account_task(w, p, nonmax);
   if (lane == 0 && (p.flags & F_STATS)) {
@@ -976,6 +981,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   const bool cbm = bm && (Wc <= 4 ? (p.narrow_qmax == 0 || nQc <= p.narrow_qmax || nQc <= p.narrow_ratio * nPc)
                                   : (nQc <= p.wide_qcap || (nQc <= p.wide_ratio * nPc && nQc <= p.wide_qmax)));
   warp_sort_pairs(w, p, nPc, nLp);
+  if ((p.flags & F_STATS) && lane == 0) tsub[3] = (unsigned long long)clock64() - tph;
   MBE_PHASE(9, tph);
   const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
                                                             : 2ull * nPc);
@@ -1022,7 +1028,17 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
   }
   publish_frame(w, p, size, nPc);
+  if ((p.flags & F_STATS) && lane == 0) tsub[4] = (unsigned long long)clock64() - tph;
   MBE_PHASE(10, tph);
+  if ((p.flags & F_STATS) && lane == 0) {  // diagnostics: remember the longest list task
+    const unsigned long long dt = (unsigned long long)clock64() - tstart;
+    if (atomicMax(&p.gl->longest[0], dt) < dt) {
+      unsigned long long* L = p.gl->longest;
+      L[1] = root ? 1ull : 0ull; L[2] = x; L[3] = dx; L[4] = nLp; L[5] = nt; L[6] = nPc; L[7] = nQc;
+      L[8] = cbm ? Wc : 0ull; L[9] = tsub[0]; L[10] = tsub[1]; L[11] = tsub[2]; L[12] = tsub[3]; L[13] = tsub[4];
+      L[14] = nQk; L[15] = nP;
+    }
+  }
 }
 
 // ================================================================== bit-row path
