@@ -391,9 +391,15 @@ __device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint
     bool valid = base + lane < n;
     Row<W> r = valid ? load_row<W>(src + (size_t)(base + lane) * W) : zero_row<W>();
     bool dom = !valid;
-    for (uint32_t k = 0; k < K; ++k) {
-      Row<W> kr = load_row<W>(dst + (size_t)k * W);
-      if (row_subset<W>(r, kr)) dom = true;
+    // kept rows in blocks of 32: one coalesced load per lane, then 32 register shuffles
+    for (uint32_t kb = 0; kb < K; kb += 32) {
+      const bool kval = kb + lane < K;
+      const Row<W> kr = kval ? load_row<W>(dst + (size_t)(kb + lane) * W) : zero_row<W>();
+      const uint32_t nk = min(32u, K - kb);
+      for (uint32_t m = 0; m < nk; ++m) {
+        const Row<W> km = shfl_row<W>(kr, (int)m);
+        if (row_subset<W>(r, km)) dom = true;
+      }
     }
     uint32_t vb = __ballot_sync(FULLMASK, valid);
 #pragma unroll 4
@@ -524,10 +530,18 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
     const uint32_t* r = src + (size_t)(valid ? t : 0) * W;
     const unsigned long long mr = valid ? wide_meta(r, W) : 0ull;
     bool dom = !valid;
-    for (uint32_t k = 0; k < K; ++k) {
-      const unsigned long long mk =
-          k < MBE_SMEM_SORT ? kmeta[k] : (kmeta_g ? kmeta_g[k] : wide_meta(dst + (size_t)k * W, W));
-      if (!dom && meta_may_subset(mr, mk) && wide_subset(r, dst + (size_t)k * W, W)) dom = true;
+    // kept rows in blocks of 32: lane l fetches the (popc, fold) of kept row kb+l, then the
+    // block is broadcast by shuffles; only pairs passing the filter stream their words
+    for (uint32_t kb = 0; kb < K; kb += 32) {
+      const uint32_t kk = kb + lane;
+      const unsigned long long mkl =
+          kk < K ? (kk < MBE_SMEM_SORT ? kmeta[kk] : (kmeta_g ? kmeta_g[kk] : wide_meta(dst + (size_t)kk * W, W)))
+                 : ~0ull;
+      const uint32_t nk = min(32u, K - kb);
+      for (uint32_t m = 0; m < nk; ++m) {
+        const unsigned long long mk = __shfl_sync(FULLMASK, mkl, (int)m);
+        if (!dom && meta_may_subset(mr, mk) && wide_subset(r, dst + (size_t)(kb + m) * W, W)) dom = true;
+      }
     }
     const uint32_t vb = __ballot_sync(FULLMASK, valid);
     for (int m = 0; m < 32; ++m) {
