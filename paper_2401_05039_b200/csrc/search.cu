@@ -489,14 +489,14 @@ __device__ __noinline__ uint32_t dedup_sort_rows(const uint32_t* src, uint32_t n
 // Same reduction for wide rows (8 or 16 words), word-sliced: rows are streamed from
 // memory (L1) instead of held in registers.
 __device__ __forceinline__ bool wide_subset(const uint32_t* a, const uint32_t* b, uint32_t W) {  // a ⊆ b
-  uint32_t x = 0;
-  for (uint32_t q = 0; q < W; ++q) x |= a[q] & ~b[q];
-  return x == 0;
+  for (uint32_t q = 0; q < W; ++q)  // early exit: most non-subset pairs fail within a word or two
+    if (a[q] & ~b[q]) return false;
+  return true;
 }
 __device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, uint32_t W) {
-  uint32_t x = 0;
-  for (uint32_t q = 0; q < W; ++q) x |= a[q] ^ b[q];
-  return x == 0;
+  for (uint32_t q = 0; q < W; ++q)
+    if (a[q] != b[q]) return false;
+  return true;
 }
 
 // Wide-row antichain with cheap necessary-condition filters: a ⊆ b requires
