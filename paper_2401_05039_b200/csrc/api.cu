@@ -624,9 +624,11 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       const unsigned long long* L = hg.longest;
       std::fprintf(stderr,
                    "longest list task: %.3f ms root=%llu x=%llu deg=%llu |L'|=%llu touched=%llu |P'|=%llu |Q'|=%llu "
-                   "Wchild=%llu kept=%llu nP=%llu | isect %.3f scan %.3f classify %.3f sort %.3f child %.3f ms\n",
+                   "Wchild=%llu kept=%llu nP=%llu | isect %.3f scan %.3f classify %.3f sort %.3f child %.3f ms "
+                   "(dedup %.3f ms -> %llu rows, antichain %.3f ms)\n",
                    L[0] / 1.965e6, L[1], L[2], L[3], L[4], L[5], L[6], L[7], L[8], L[14], L[15], L[9] / 1.965e6,
-                   L[10] / 1.965e6, L[11] / 1.965e6, L[12] / 1.965e6, L[13] / 1.965e6);
+                   L[10] / 1.965e6, L[11] / 1.965e6, L[12] / 1.965e6, L[13] / 1.965e6, L[16] / 1.965e6, L[18],
+                   L[17] / 1.965e6);
     }
     res->roots_out_ms = hg.t_roots_out == ~0ull ? -1.0 : (double)hg.t_roots_out * 1e-6;
     if (cfg.per_root) {

@@ -52,7 +52,7 @@ struct Globals {
   unsigned long long max_task[4];  // MBE_STATS: longest single task (cycles): root, list, bit-row, -
   unsigned long long t_roots_out;  // MBE_STATS: ns after launch when the level-1 list ran out
   unsigned long long max_phase[16];  // MBE_STATS: longest single occurrence of each sub-phase (cycles)
-  unsigned long long longest[16];    // MBE_STATS diagnostics: the longest list-path task (see search.cu)
+  unsigned long long longest[20];    // MBE_STATS diagnostics: the longest list-path task (see search.cu)
 };
 
 struct SearchParams {

@@ -781,6 +781,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
   const unsigned long long tstart = tph;
   unsigned long long tsub[5] = {0, 0, 0, 0, 0};
+  unsigned long long tdd[3] = {0, 0, 0};
   // Step 2: L' = L ∩ N(x)
   const uint32_t* Lp;
   uint32_t nLp;
@@ -943,15 +944,27 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
     nRx += __popc(be);
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
-    // words 4.. of a wide (8/16-word) row are still in the slot: copied, then cleared below
+    // words 4.. of a wide (8/16-word) row are still in the slot extension: staged in registers
+    // with vector loads (one round trip), copied to the candidate buffers, then cleared
     uint32_t* ex = w.sext + (size_t)v * MBE_SEXT_WORDS;
+    uint32_t exw[MBE_SEXT_WORDS];
+    if (Wc > 4 && valid) {
+      const uint4* e4 = reinterpret_cast<const uint4*>(ex);
+      const uint4 e0 = e4[0];
+      exw[0] = e0.x; exw[1] = e0.y; exw[2] = e0.z; exw[3] = e0.w;
+      if (Wc > 8) {
+        const uint4 e1 = e4[1], e2 = e4[2];
+        exw[4] = e1.x; exw[5] = e1.y; exw[6] = e1.z; exw[7] = e1.w;
+        exw[8] = e2.x; exw[9] = e2.y; exw[10] = e2.z; exw[11] = e2.w;
+      }
+    }
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
       w.skey[idx] = ((unsigned long long)c << 32) | v;
       w.sval[idx] = idx;
       if (bm) {
         for (uint32_t q = 0; q < Wc && q < 4; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
-        for (uint32_t q = 4; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = ex[q - 4];
+        for (uint32_t q = 4; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = exw[q - 4];
       }
     }
     nPc += __popc(bp);
@@ -960,11 +973,17 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       if (isQ) {
         uint32_t idx = nQc + __popc(bq & lanemask_lt());
         for (uint32_t q = 0; q < Wc && q < 4; ++q) w.qbuf[(size_t)idx * Wc + q] = rw[q];
-        for (uint32_t q = 4; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = ex[q - 4];
+        for (uint32_t q = 4; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = exw[q - 4];
       }
       nQc += __popc(bq);
-      if (Wc > 4 && valid)
-        for (uint32_t q = 4; q < Wc; ++q) ex[q - 4] = 0u;
+      if (Wc > 4 && valid) {
+        uint4* e4 = reinterpret_cast<uint4*>(ex);
+        e4[0] = make_uint4(0u, 0u, 0u, 0u);
+        if (Wc > 8) {
+          e4[1] = make_uint4(0u, 0u, 0u, 0u);
+          e4[2] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
     }
       }
   }
@@ -1019,12 +1038,22 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     __syncwarp();
     const uint32_t* qsrc = w.qbuf;
     uint32_t qn = nQc;
+    const unsigned long long td0 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
     if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
       qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
                            w.sm, lane);
       qsrc = w.pbuf;
     }
-    nQk = antichain_w(Wc, qsrc, qn, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm, w.skey);
+    const unsigned long long td1 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+    // wide rows with many distinct Q' rows: keep the (exactly deduplicated) rows without the
+    // O(n * K) antichain pass; extra dominated rows never change a maximality decision
+    const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256);
+    nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey);
+    if (p.flags & F_STATS) {
+      tdd[0] = td1 - td0;
+      tdd[1] = (unsigned long long)clock64() - td1;
+      tdd[2] = qn;
+    }
     size = (uint64_t)(CQ + (size_t)nQk * Wc - C);
   } else {
     uint32_t* CK = CP + nPc;
@@ -1050,7 +1079,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       unsigned long long* L = p.gl->longest;
       L[1] = root ? 1ull : 0ull; L[2] = x; L[3] = dx; L[4] = nLp; L[5] = nt; L[6] = nPc; L[7] = nQc;
       L[8] = cbm ? Wc : 0ull; L[9] = tsub[0]; L[10] = tsub[1]; L[11] = tsub[2]; L[12] = tsub[3]; L[13] = tsub[4];
-      L[14] = nQk; L[15] = nP;
+      L[14] = nQk; L[15] = nP; L[16] = tdd[0]; L[17] = tdd[1]; L[18] = tdd[2];
     }
   }
 }
@@ -1290,7 +1319,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
       bool sub = valid;
       if (valid) {
         const uint32_t* r = Qrow + (size_t)(qb + lane) * W;
-        for (uint32_t q = 0; q < W; ++q) sub &= (lx[q] & ~r[q]) == 0u;
+        for (uint32_t q = 0; q < W && sub; ++q) sub = (lx[q] & ~r[q]) == 0u;
       }
       if (__any_sync(FULLMASK, sub)) {
         nonmax = true;
