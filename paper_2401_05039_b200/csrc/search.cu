@@ -39,11 +39,13 @@ namespace {
 #define SM_PROW_WORDS 128
 #define SM_QROW_WORDS 256
 #define SM_RBUF 128
-#define FC_WORDS 640  // shared-memory copy of the warp's top frame (owner reads only)
+#define FC_WORDS 448  // shared-memory copy of the warp's top frame (owner reads only)
 struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligned offset
-  unsigned long long skey[MBE_SMEM_SORT];
+  union {                               // never live at the same time:
+    unsigned long long skey[MBE_SMEM_SORT];  //   small sorts, antichain staging / wide metadata
+    unsigned int hist[256];                  //   radix-sort histogram (keys then live in HBM)
+  };
   unsigned int sval[MBE_SMEM_SORT];
-  unsigned int hist[256];
   unsigned int foff[MBE_MAXDEPTH];  // arena word offset of the frame at each depth
   unsigned int fnp[MBE_MAXDEPTH];   // its task limit (|P|, or the end of a stolen range)
   unsigned int ffirst[MBE_MAXDEPTH];  // first task of its range (0 unless a thief's copy)
