@@ -382,7 +382,8 @@ __device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint
 // "∃q: L'' ⊆ N(q)" holds for a dominated row only if it holds for its
 // dominator.  With keep_all, rows are copied unchanged.
 template <int W>
-__device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane) {
+__device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint32_t* dst, bool keep_all, int lane,
+                                           bool sorted_desc = false) {
   if (keep_all) {
     for (uint32_t t = lane; t < n; t += 32) store_row<W>(dst + (size_t)t * W, load_row<W>(src + (size_t)t * W));
     __syncwarp();
@@ -411,7 +412,12 @@ __device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint
     }
     bool surv = valid && !dom;
     uint32_t bs = __ballot_sync(FULLMASK, surv);
-    if (bs) {
+    if (bs && sorted_desc) {
+      // candidates arrive by descending popcount: a survivor cannot strictly contain a kept row
+      if (surv) store_row<W>(dst + (size_t)(K + __popc(bs & lanemask_lt())) * W, r);
+      K += __popc(bs);
+      __syncwarp();
+    } else if (bs) {
       uint32_t newK = 0;
       for (uint32_t kb = 0; kb < K; kb += 32) {
         bool kval = kb + lane < K;
@@ -600,12 +606,43 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
   return K;
 }
 
+// Rows reordered by descending popcount (counting sort; order inside a popcount is arbitrary).
+// hist: shared memory with >= 32*W + 1 entries.
+__device__ __noinline__ void popc_sort_rows_desc(const uint32_t* src, uint32_t n, uint32_t W, uint32_t* dst,
+                                                 uint32_t* hist, int lane) {
+  const uint32_t nb = 32 * W + 1;
+  for (uint32_t b = lane; b < nb; b += 32) hist[b] = 0;
+  __syncwarp();
+  for (uint32_t t = lane; t < n; t += 32) {
+    uint32_t pc = 0;
+    for (uint32_t q = 0; q < W; ++q) pc += __popc(src[(size_t)t * W + q]);
+    atomicAdd(&hist[32 * W - pc], 1u);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    uint32_t run = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      const uint32_t c = hist[b];
+      hist[b] = run;
+      run += c;
+    }
+  }
+  __syncwarp();
+  for (uint32_t t = lane; t < n; t += 32) {
+    uint32_t pc = 0;
+    for (uint32_t q = 0; q < W; ++q) pc += __popc(src[(size_t)t * W + q]);
+    const uint32_t pos = atomicAdd(&hist[32 * W - pc], 1u);
+    for (uint32_t q = 0; q < W; ++q) dst[(size_t)pos * W + q] = src[(size_t)t * W + q];
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ uint32_t antichain_w(uint32_t Wc, const uint32_t* src, uint32_t n, uint32_t* dst,
                                                 bool keep_all, int lane, WarpSmem* sm,
-                                                unsigned long long* kmeta_g = nullptr) {
-  if (Wc == 1) return antichain<1>(src, n, dst, keep_all, lane);
-  if (Wc == 2) return antichain<2>(src, n, dst, keep_all, lane);
-  if (Wc == 4) return antichain<4>(src, n, dst, keep_all, lane);
+                                                unsigned long long* kmeta_g = nullptr, bool sorted_desc = false) {
+  if (Wc == 1) return antichain<1>(src, n, dst, keep_all, lane, sorted_desc);
+  if (Wc == 2) return antichain<2>(src, n, dst, keep_all, lane, sorted_desc);
+  if (Wc == 4) return antichain<4>(src, n, dst, keep_all, lane, sorted_desc);
   return antichain_wide(src, n, dst, Wc, keep_all, lane, sm->skey, kmeta_g);
 }
 
@@ -1050,7 +1087,13 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     // wide rows with many distinct Q' rows: keep the (exactly deduplicated) rows without the
     // O(n * K) antichain pass; extra dominated rows never change a maximality decision
     const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256);
-    nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey);
+    bool sorted = qsrc == w.pbuf;  // dedup output is in descending popcount order
+    if (!keep_all && !sorted && Wc <= 4 && qn > 128) {
+      popc_sort_rows_desc(qsrc, qn, Wc, w.pbuf, w.sm->sval, lane);
+      qsrc = w.pbuf;
+      sorted = true;
+    }
+    nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey, sorted);
     if (p.flags & F_STATS) {
       tdd[0] = td1 - td0;
       tdd[1] = (unsigned long long)clock64() - td1;
