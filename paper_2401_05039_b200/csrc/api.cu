@@ -540,6 +540,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       p.narrow_qmax = nq ? (uint32_t)std::strtoul(nq, nullptr, 10) : 0u;
       const char* nr = std::getenv("MBE_NARROW_RATIO");
       p.narrow_ratio = nr ? (uint32_t)std::strtoul(nr, nullptr, 10) : 256u;
+      const char* am = std::getenv("MBE_AC_MIN");
+      p.ac_min = am ? (uint32_t)std::strtoul(am, nullptr, 10) : 1024u;
+      const char* ar = std::getenv("MBE_AC_RATIO");
+      p.ac_ratio = ar ? (uint32_t)std::strtoul(ar, nullptr, 10) : 64u;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
       p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 8192u;
     }

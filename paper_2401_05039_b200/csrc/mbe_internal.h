@@ -63,7 +63,8 @@ struct SearchParams {
   uint32_t wide_ratio;  //   ... or |Q'| <= wide_ratio * |P'| and |Q'| <= wide_qmax
   uint32_t wide_qmax;
   uint32_t narrow_qmax, narrow_ratio;  // same guard for 1/2/4-word children (narrow_qmax 0 = always)
-  uint32_t dedup_min;   // list-path children with more Q' candidates are deduplicated before the antichain
+  uint32_t dedup_min;
+  uint32_t ac_min, ac_ratio;  // list-path children skip the antichain if |Q'| > ac_min and > ac_ratio*(|P'|+1)   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;
   uint32_t rank, world;
   unsigned long long* claim_counter;  // NULL -> static deal

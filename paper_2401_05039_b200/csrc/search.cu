@@ -1086,13 +1086,11 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     const unsigned long long td1 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
     // wide rows with many distinct Q' rows: keep the (exactly deduplicated) rows without the
     // O(n * K) antichain pass; extra dominated rows never change a maximality decision
-    const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256);
-    bool sorted = qsrc == w.pbuf;  // dedup output is in descending popcount order
-    if (!keep_all && !sorted && Wc <= 4 && qn > 128) {
-      popc_sort_rows_desc(qsrc, qn, Wc, w.pbuf, w.sm->sval, lane);
-      qsrc = w.pbuf;
-      sorted = true;
-    }
+    // The antichain is one warp's serial O(n * K) pass; when Q' is far larger than the number of
+    // sibling tasks that will read it, keeping the rows unreduced is cheaper (exact either way).
+    const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256) ||
+                          (qn > p.ac_min && qn > p.ac_ratio * (nPc + 1));
+    const bool sorted = qsrc == w.pbuf;  // dedup output is in descending popcount order
     nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey, sorted);
     if (p.flags & F_STATS) {
       tdd[0] = td1 - td0;
