@@ -148,14 +148,14 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle (cpu_baseline / reference arm)
-def oracle_rate(g, target_s: float, seed: int = 7):
-    """Oracle bicliques/s on a bounded, representative sample of level-1 subtrees.
+def oracle_rate(g, target_s: float, seed: int = 7, config: str = ""):
+    """Oracle bicliques/s on a bounded sample of level-1 subtrees.
 
-    Per-root oracle cost is heavy-tailed, so the sample is systematic: roots sorted by a cost proxy
-    (the size of their 2-hop neighbourhood), every k-th taken (offset from the seed), and run as ONE
-    oracle call so its threads schedule heavy and light roots together.  The heaviest 1% of roots by
-    the proxy are excluded to keep the time bounded (this can only flatter the CPU number).  k is
-    calibrated by a pilot run of ~1/400 of the roots so that the timed sample takes ~target_s seconds.
+    Per-root oracle cost is extremely heavy-tailed: on C2/C5 the heaviest 1% of roots (by 2-hop
+    size) hold ~90-95% of the oracle's work and single roots take minutes, so no small sample that
+    includes them has a bounded time.  The sample therefore EXCLUDES the heaviest 1% and takes every
+    k-th remaining root in cost order, as ONE oracle call (k calibrated by a pilot to ~target_s).
+    This flatters the CPU (several-fold); the recorded full-run oracle time is reported beside it.
     """
     import oracle
 
@@ -166,22 +166,22 @@ def oracle_rate(g, target_s: float, seed: int = 7):
     cand, other = (e[:, 0], e[:, 1]) if side == 1 else (e[:, 1], e[:, 0])
     deg_other = np.bincount(other, minlength=g.n2 if side == 1 else g.n1)
     proxy = np.bincount(cand, weights=deg_other[other], minlength=n)
-    order = np.argsort(proxy, kind="stable").astype(np.uint32)
-    order = order[: max(1, int(n * 0.99))]  # drop the 1% heaviest roots (bounded time; flatters the CPU)
-    off = seed % 997
+    order = np.argsort(proxy, kind="stable").astype(np.uint32)[: max(1, int(n * 0.99))]
 
     def run(k):
-        roots = order[(off % k)::k]
+        roots = order[(seed % k)::k]
         t0 = time.perf_counter()
         pr = oracle.mbea_roots(g, roots, candidate_side=side)
         return int(pr[:, 0].sum()), time.perf_counter() - t0, len(roots)
 
-    k = max(1, n // 400)
+    k = max(1, len(order) // 400)
     cnt, dt, m = run(k)
-    if dt < 0.5 * target_s and k > 1:
+    for _ in range(3):
+        if dt >= 0.5 * target_s or k == 1:
+            break
         k = max(1, int(k * dt / target_s))
         cnt, dt, m = run(k)
-    return cnt / dt, dict(count=cnt, seconds=dt, roots=m, frac=m / n, threads=threads, side=side)
+    return cnt / dt, dict(count=cnt, seconds=dt, roots=m, frac=m / n, threads=threads, side=side, k=k)
 
 
 def golden_full_run(config):
@@ -208,20 +208,21 @@ def run_reference(args):
     per_step_target = max(3.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
     rates, infos = [], []
     for s in range(args.warmup + args.steps):
-        r, info = oracle_rate(g, per_step_target, seed=7 + s)
+        r, info = oracle_rate(g, per_step_target, seed=7 + s, config=args.config)
         if s >= args.warmup:
             rates.append(r)
             infos.append(info)
     value = float(np.mean(rates))
     info = infos[-1]
-    sample = (f"{info['roots']} of the level-1 subtrees ({100 * info['frac']:.2f}%: every k-th root in 2-hop-size "
-              f"order excluding the heaviest 1%), {info['count']} bicliques in {info['seconds']:.1f} s per step")
+    sample = (f"{info['roots']} of the level-1 subtrees ({100 * info['frac']:.2f}%: every {info['k']}-th root in 2-hop-size "
+              f"order, heaviest 1% excluded), {info['count']} bicliques in {info['seconds']:.1f} s per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([i["seconds"] for i in infos])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": WORKLOADS.get(args.config, args.config), "parallelism": "CPU threads over level-1 subtrees"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["threads"], "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["threads"], "kind": "oracle", "sample": sample,
+                         "full_run": golden_full_run(args.config)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -338,11 +339,11 @@ def run_ours(args):
         import oracle
 
         oracle.build_oracle()
-        rate, info = oracle_rate(g, args.cpu_seconds)
+        rate, info = oracle_rate(g, args.cpu_seconds, config=args.config)
         full = golden_full_run(args.config)
         cpu = {"value": rate, "unit": UNIT, "cores": info["threads"], "kind": "oracle", "full_run": full,
-               "sample": f"{info['roots']} level-1 subtrees ({100 * info['frac']:.2f}%: every k-th root in 2-hop-size "
-                         f"order excluding the heaviest 1%, one oracle call), {info['count']} bicliques in {info['seconds']:.1f} s"}
+               "sample": f"{info['roots']} level-1 subtrees ({100 * info['frac']:.2f}%: every {info['k']}-th root in "
+                         f"2-hop-size order, heaviest 1% excluded, one oracle call), {info['count']} bicliques in {info['seconds']:.1f} s"}
     if rank == 0:
         total_warps = st.n_warps
         line = {
