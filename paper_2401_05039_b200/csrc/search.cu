@@ -293,10 +293,12 @@ __device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, 
   int np = 0;
   for (uint32_t s = 0; s < id_bits; s += 8) shifts[np++] = s;
   for (uint32_t s = 0; s < cnt_bits; s += 8) shifts[np++] = 32 + s;
+#pragma unroll 1
   for (int pass = 0; pass < np; ++pass) {
     uint32_t sh = shifts[pass];
     for (int b = lane; b < 256; b += 32) sm->hist[b] = 0;
     __syncwarp();
+#pragma unroll 1
     for (uint32_t t = lane; t < n; t += 32) atomicAdd(&sm->hist[(src_k[t] >> sh) & 255u], 1u);
     __syncwarp();
     // exclusive scan of 256 buckets: lane owns 8 consecutive buckets
@@ -321,6 +323,7 @@ __device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, 
       run += loc[q];
     }
     __syncwarp();
+#pragma unroll 1
     for (uint32_t base = 0; base < n; base += 32) {
       uint32_t t = base + lane;
       bool valid = t < n;
@@ -346,6 +349,7 @@ __device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, 
     dst_v = tv;
   }
   if (src_k != key) {
+#pragma unroll 1
     for (uint32_t t = lane; t < n; t += 32) {
       key[t] = src_k[t];
       val[t] = src_v[t];
