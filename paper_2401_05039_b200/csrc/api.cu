@@ -66,10 +66,39 @@ struct Side {
   uint32_t nU = 0, nV = 0, n_roots = 0, maxdegU = 0;
   std::vector<uint32_t> origU;  // host copy: rank -> original id
   std::vector<uint32_t> rankU;  // host copy: original id -> rank
-  DevBuf offU, adjU, offV, adjV, hvU, hvV, origUd, root_order, twin;
+  DevBuf all;                   // one device allocation holding every array below
+  DevBuf offU, adjU, offV, adjV, hvU, hvV, origUd, root_order, twin;  // views into `all` (not owned)
   void release() {
-    for (DevBuf* b : {&offU, &adjU, &offV, &adjV, &hvU, &hvV, &origUd, &root_order, &twin}) b->release();
+    all.release();
+    for (DevBuf* b : {&offU, &adjU, &offV, &adjV, &hvU, &hvV, &origUd, &root_order, &twin}) *b = DevBuf();
     built = false;
+  }
+};
+
+// Packs host arrays into one device allocation (one cudaMalloc, one cudaFree per side).
+struct Packer {
+  struct Item { DevBuf* dst; const void* src; size_t bytes; size_t off; };
+  std::vector<Item> items;
+  size_t total = 0;
+  void add(DevBuf& dst, const void* src, size_t bytes) {
+    items.push_back({&dst, src, bytes, total});
+    total += (std::max<size_t>(bytes, 16) + 255) & ~size_t(255);
+  }
+  int commit(DevBuf& all, uint64_t* counter) {
+    if (cudaMalloc(&all.p, std::max<size_t>(total, 256)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MBE_ENOMEM, "cudaMalloc graph");
+    }
+    all.bytes = total;
+    std::vector<uint8_t> host(total);
+    for (const Item& it : items) {
+      if (it.src && it.bytes) std::memcpy(host.data() + it.off, it.src, it.bytes);
+      it.dst->p = static_cast<uint8_t*>(all.p) + it.off;
+      it.dst->bytes = it.bytes;
+      if (counter && it.src) *counter += it.bytes;
+    }
+    CUDA_TRY(cudaMemcpy(all.p, host.data(), total, cudaMemcpyHostToDevice));
+    return MBE_OK;
   }
 };
 
@@ -179,16 +208,20 @@ int build_side(mbe_graph* g, int s) {
   std::vector<uint32_t> order(cost.size());
   for (size_t k = 0; k < cost.size(); ++k) order[k] = cost[k].second;
   S.n_roots = (uint32_t)order.size();
-  int rc;
-  if ((rc = upload(S.offU, offU)) || (rc = upload(S.adjU, adjU)) || (rc = upload(S.offV, offV)) ||
-      (rc = upload(S.adjV, adjV)) || (rc = upload(S.hvU, hvU)) || (rc = upload(S.hvV, hvV)) ||
-      (rc = upload(S.origUd, S.origU)) || (rc = upload(S.root_order, order))) {
+  Packer pk;
+  pk.add(S.offU, offU.data(), offU.size() * 4);
+  pk.add(S.adjU, adjU.data(), adjU.size() * 4);
+  pk.add(S.offV, offV.data(), offV.size() * 4);
+  pk.add(S.adjV, adjV.data(), adjV.size() * 4);
+  pk.add(S.hvU, hvU.data(), hvU.size() * 8);
+  pk.add(S.hvV, hvV.data(), hvV.size() * 8);
+  pk.add(S.origUd, S.origU.data(), S.origU.size() * 4);
+  pk.add(S.root_order, order.data(), order.size() * 4);
+  pk.add(S.twin, nullptr, nU);  // written by the twin pre-pass
+  int rc = pk.commit(S.all, g_upload_counter);
+  if (rc) {
     S.release();
     return rc;
-  }
-  if (cudaMalloc(&S.twin.p, std::max<size_t>(nU, 16)) != cudaSuccess) {
-    S.release();
-    return fail(MBE_ENOMEM, "cudaMalloc twin");
   }
   S.built = true;
   return MBE_OK;
@@ -359,7 +392,7 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
   for (uint32_t i = 0; i < n1; ++i) {
     size_t b = g->adj1.size();
     g->adj1.insert(g->adj1.end(), col_idx + row_ptr[i], col_idx + row_ptr[i + 1]);
-    std::sort(g->adj1.begin() + b, g->adj1.end());
+    if (!std::is_sorted(g->adj1.begin() + b, g->adj1.end())) std::sort(g->adj1.begin() + b, g->adj1.end());
     g->adj1.erase(std::unique(g->adj1.begin() + b, g->adj1.end()), g->adj1.end());
     g->off1[i + 1] = (uint32_t)g->adj1.size();
   }
@@ -374,12 +407,10 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
     for (uint32_t i = 0; i < n1; ++i)
       for (uint32_t e = g->off1[i]; e < g->off1[i + 1]; ++e) g->adj2[fill[g->adj1[e]]++] = i;
   }
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+  if (cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
     delete g;
-    return fail(MBE_ECUDA, "cudaGetDeviceProperties");
+    return fail(MBE_ECUDA, "cudaDeviceGetAttribute(multiProcessorCount)");
   }
-  g->sm_count = prop.multiProcessorCount;
   if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) {
     delete g;
     return fail(MBE_ECUDA, "cudaEventCreate");
