@@ -148,6 +148,14 @@ int build_side(mbe_graph* g, int s) {
   Side& S = g->side[s - 1];
   if (S.built) return MBE_OK;
   g_upload_counter = &g->h2d_bytes;
+  const bool dbg = std::getenv("MBE_DEBUG_TIMING") != nullptr;
+  auto T = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "    side %-26s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - T).count());
+    T = n;
+  };
   const std::vector<uint32_t>& offC = s == 1 ? g->off1 : g->off2;  // candidate side CSR
   const std::vector<uint32_t>& adjC = s == 1 ? g->adj1 : g->adj2;
   const uint32_t nU = s == 1 ? g->n1 : g->n2, nV = s == 1 ? g->n2 : g->n1;
@@ -167,6 +175,7 @@ int build_side(mbe_graph* g, int s) {
     S.rankU[u] = r;
   }
   S.maxdegU = maxdeg;
+  lap("relabel");
   // adjU[rank] = sorted V ids; adjV[v] = sorted ranks
   std::vector<uint32_t> offU(nU + 1, 0), adjU(g->nE), offV(nV + 1, 0), adjV(g->nE);
   for (uint32_t r = 0; r < nU; ++r) {
@@ -176,37 +185,42 @@ int build_side(mbe_graph* g, int s) {
   }
   for (uint64_t e = 0; e < g->nE; ++e) offV[adjU[e] + 1]++;
   for (uint32_t v = 0; v < nV; ++v) offV[v + 1] += offV[v];
+  // execution-order cost of each level-1 subtree (descending P-role 2-hop estimate):
+  //   cost(x) = Σ_{u ∈ N(x)} |{w ∈ N(u) : w > x}|
+  // filled in rank order, x lands at position k of adjV[u], so the term is deg(u) - k - 1 (O(E)).
+  std::vector<uint64_t> rcost(nU, 0);
   {
     std::vector<uint32_t> fill(offV.begin(), offV.end() - 1);
-    for (uint32_t r = 0; r < nU; ++r)
-      for (uint32_t e = offU[r]; e < offU[r + 1]; ++e) adjV[fill[adjU[e]]++] = r;
+    for (uint32_t r = 0; r < nU; ++r) {
+      uint64_t c = 0;
+      for (uint32_t e = offU[r]; e < offU[r + 1]; ++e) {
+        const uint32_t u = adjU[e];
+        const uint32_t k = fill[u]++;
+        adjV[k] = r;
+        c += offV[u + 1] - k - 1;
+      }
+      rcost[r] = c;
+    }
   }
+  lap("adjacency");
   // hash terms: side bit 0 for side 1 (rows), 1 for side 2 (cols)
   std::vector<uint64_t> hvU(nU), hvV(nV);
   const uint64_t bu = s == 1 ? 0 : 1, bv = 1 - bu;
   for (uint32_t r = 0; r < nU; ++r) hvU[r] = mbe_mix64(2ull * S.origU[r] + bu);
   for (uint32_t v = 0; v < nV; ++v) hvV[v] = mbe_mix64(2ull * v + bv);
-  // execution order of level-1 subtrees: descending P-role 2-hop estimate
-  //   cost(x) = Σ_{u ∈ N(x)} |{w ∈ N(u) : w > x}|, ties by rank
-  std::vector<std::pair<uint64_t, uint32_t>> cost;
-  cost.reserve(nU);
+  lap("hash terms");
+  // execution order: descending cost, ties by rank (one u64 key per root)
+  std::vector<uint64_t> key;
+  key.reserve(nU);
   for (uint32_t r = 0; r < nU; ++r) {
     if (offU[r + 1] == offU[r]) continue;
-    uint64_t c = 0;
-    for (uint32_t e = offU[r]; e < offU[r + 1]; ++e) {
-      uint32_t u = adjU[e];
-      const uint32_t* b = adjV.data() + offV[u];
-      const uint32_t* en = adjV.data() + offV[u + 1];
-      c += (uint64_t)(en - std::upper_bound(b, en, r));
-    }
-    cost.push_back({c, r});
+    const uint64_t c = std::min<uint64_t>(rcost[r], 0xffffffffull);
+    key.push_back(((0xffffffffull - c) << 32) | r);
   }
-  std::sort(cost.begin(), cost.end(), [](const std::pair<uint64_t, uint32_t>& a, const std::pair<uint64_t, uint32_t>& b) {
-    if (a.first != b.first) return a.first > b.first;
-    return a.second < b.second;
-  });
-  std::vector<uint32_t> order(cost.size());
-  for (size_t k = 0; k < cost.size(); ++k) order[k] = cost[k].second;
+  std::sort(key.begin(), key.end());
+  lap("root cost + sort");
+  std::vector<uint32_t> order(key.size());
+  for (size_t k = 0; k < key.size(); ++k) order[k] = (uint32_t)key[k];
   S.n_roots = (uint32_t)order.size();
   Packer pk;
   pk.add(S.offU, offU.data(), offU.size() * 4);
@@ -223,6 +237,7 @@ int build_side(mbe_graph* g, int s) {
     S.release();
     return rc;
   }
+  lap("pack + upload");
   S.built = true;
   return MBE_OK;
 }
@@ -358,6 +373,14 @@ const char* mbe_last_error_detail(void) { return g_detail.c_str(); }
 
 int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32_t* col_idx, int device,
                  uint32_t flags, mbe_graph** out) {
+  const bool dbg = std::getenv("MBE_DEBUG_TIMING") != nullptr;
+  auto T = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  load %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - T).count());
+    T = n;
+  };
   (void)flags;
   if (!out) return fail(MBE_EINVAL, "out is NULL");
   *out = nullptr;
@@ -374,6 +397,7 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
       return fail(MBE_ERANGE, "row " + std::to_string(row) + ": col " + std::to_string(col_idx[e]) +
                                   " >= n2=" + std::to_string(n2));
     }
+  lap("validate");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -397,6 +421,7 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
     g->off1[i + 1] = (uint32_t)g->adj1.size();
   }
   g->nE = g->adj1.size();
+  lap("row CSR sort+dedup");
   // column CSR (counting sort; rows visited ascending -> sorted)
   g->off2.assign(n2 + 1, 0);
   g->adj2.resize(g->nE);
@@ -407,6 +432,7 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
     for (uint32_t i = 0; i < n1; ++i)
       for (uint32_t e = g->off1[i]; e < g->off1[i + 1]; ++e) g->adj2[fill[g->adj1[e]]++] = i;
   }
+  lap("column CSR");
   if (cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
     delete g;
     return fail(MBE_ECUDA, "cudaDeviceGetAttribute(multiProcessorCount)");
@@ -415,12 +441,14 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
     delete g;
     return fail(MBE_ECUDA, "cudaEventCreate");
   }
+  lap("device attr + events");
   int side = n2 < n1 ? 2 : 1;
   int rc = build_side(g, side);
   if (rc) {
     delete g;
     return rc;
   }
+  lap("build_side (relabel, hv, order, upload)");
   *out = g;
   return MBE_OK;
 }
