@@ -1733,27 +1733,46 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       // Fast path: most tasks are 1-word bit-row tasks pruned by the maximality check (SURVEY
       // fact 8); decide those here with a few shared-memory reads, outside the general task
       // code, so the hot instruction stream stays small.
-      if (F == w.sm->fcache && F[0] == (KIND_BITMAP | (1u << 8)) && w1_pruned(F, i, lane)) {
-        if (lane == 0) {
-          w.tasks++;
-          w.pruned++;
-          if (p.per_root) {
-            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 2], 1ull);
-            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 3], 1ull);
+      if (F == w.sm->fcache && F[0] == (KIND_BITMAP | (1u << 8))) {
+        // consume the rest of the claimed batch here while tasks keep getting pruned
+        uint32_t npr = 0;
+        bool maximal = false;
+        for (;;) {
+          if (!w1_pruned(F, i, lane)) {
+            maximal = true;
+            break;
           }
-          atomicAdd(&dsc->done, 1u);
-          if (nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
+          ++npr;
+          uint32_t nx = PEND_NONE;
+          if (lane == 0 && w.sm->bcur[d] < w.sm->bend[d]) nx = w.sm->bcur[d]++;
+          nx = __shfl_sync(FULLMASK, nx, 0);
+          if (nx == PEND_NONE) break;
+          i = nx;
+        }
+        if (lane == 0 && npr) {
+          w.tasks += npr;
+          w.pruned += npr;
+          if (p.per_root) {
+            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 2], (unsigned long long)npr);
+            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 3], (unsigned long long)npr);
+          }
+          atomicAdd(&dsc->done, npr);
           if (p.flags & F_STATS) {
-            w.bitmap_tasks++;
+            w.bitmap_tasks += npr;
             const uint32_t nP_ = F[2], nQ_ = F[3];
-            w.alg_bytes += 4ull * (1ull + nP_ + nQ_) + 4ull * nP_;
+            w.alg_bytes += (unsigned long long)npr * (4ull * (1ull + nP_ + nQ_) + 4ull * nP_);
             const unsigned long long dt = clock64() - t0;
             w.sm->ph[2] += dt;
             w.sm->ph[11] += dt;
+            t0 = clock64();
           }
         }
-        __syncwarp();
-        continue;
+        if (!maximal) {
+          if (lane == 0 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
+          __syncwarp();
+          continue;
+        }
+        ti = i;  // the maximal task runs through the general path below
       }
     } else if (!roots_done) {
       // ---- empty stack: next level-1 subtree (coarse-grained task)
