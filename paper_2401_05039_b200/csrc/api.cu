@@ -604,7 +604,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       const char* ar = std::getenv("MBE_AC_RATIO");
       p.ac_ratio = ar ? (uint32_t)std::strtoul(ar, nullptr, 10) : 0xffffffffu;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
-      p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 8192u;
+      p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 512u;
     }
     p.flags = cfg.flags;
     p.rank = cfg.rank;

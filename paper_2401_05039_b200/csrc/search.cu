@@ -498,6 +498,58 @@ __device__ __noinline__ uint32_t dedup_sort_rows(const uint32_t* src, uint32_t n
   return m;
 }
 
+// Exact duplicate removal by hashing (O(n), one table round trip per row).
+// table: 2^cap_log2 >= 2n u64 entries of scratch (cleared here first).
+// Entry = (hash32 << 32) | (row index + 1), claimed by CAS; on a hash match the
+// rows are compared word by word, so the result is exact.  Output rows keep
+// first-occurrence order; returns the number of distinct rows.
+__device__ __noinline__ uint32_t dedup_hash_rows(const uint32_t* src, uint32_t n, uint32_t W, uint32_t* dst,
+                                                 unsigned long long* table, uint32_t cap_log2, int lane) {
+  const uint32_t cap = 1u << cap_log2, mask = cap - 1;
+  for (uint32_t k = lane; k < cap; k += 32) table[k] = 0ull;
+  __syncwarp();
+  uint32_t m = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t t = base + lane;
+    bool keep = false;
+    if (t < n) {
+      const uint32_t* r = src + (size_t)t * W;
+      uint32_t h = 0x9E3779B9u;
+      for (uint32_t q = 0; q < W; ++q) {
+        h = (h ^ r[q]) * 0x01000193u;
+        h ^= h >> 15;
+      }
+      h = h * 0x85EBCA6Bu;
+      h ^= h >> 13;
+      const unsigned long long mine = ((unsigned long long)h << 32) | (t + 1);
+      uint32_t slot = h & mask;
+      for (;;) {
+        const unsigned long long old = atomicCAS(&table[slot], 0ull, mine);
+        if (old == 0ull) {
+          keep = true;
+          break;
+        }
+        if ((uint32_t)(old >> 32) == h) {
+          const uint32_t* o = src + (size_t)((uint32_t)old - 1) * W;
+          bool eq = true;
+          for (uint32_t q = 0; q < W && eq; ++q) eq = o[q] == r[q];
+          if (eq) break;  // duplicate of an earlier-inserted row
+        }
+        slot = (slot + 1) & mask;
+      }
+    }
+    const uint32_t bk = __ballot_sync(FULLMASK, keep);
+    if (keep) {
+      const uint32_t* r = src + (size_t)t * W;
+      uint32_t* o = dst + (size_t)(m + __popc(bk & lanemask_lt())) * W;
+      for (uint32_t q = 0; q < W; ++q) o[q] = r[q];
+    }
+    m += __popc(bk);
+  }
+  __syncwarp();
+  return m;
+}
+
 // Same reduction for wide rows (8 or 16 words), word-sliced: rows are streamed from
 // memory (L1) instead of held in registers.
 __device__ __forceinline__ bool wide_subset(const uint32_t* a, const uint32_t* b, uint32_t W) {  // a ⊆ b
@@ -1052,8 +1104,15 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     uint32_t qn = nQc;
     const unsigned long long td0 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
     if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
-      qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
-                           w.sm, lane);
+      // hash table in the (now free) sort-key scratch: 2 x nU u64 entries, power of two >= 2 nQc
+      uint32_t lg = 1;
+      while ((1u << lg) < 2 * nQc) ++lg;
+      if ((1ull << lg) <= 2ull * p.skey2_off) {
+        qn = dedup_hash_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, lg, lane);
+      } else {
+        qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
+                             w.sm, lane);
+      }
       qsrc = w.pbuf;
     }
     const unsigned long long td1 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
@@ -1063,7 +1122,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     // sibling tasks that will read it, keeping the rows unreduced is cheaper (exact either way).
     const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256) ||
                           (qn > p.ac_min && qn > p.ac_ratio * (nPc + 1));
-    const bool sorted = qsrc == w.pbuf;  // dedup output is in descending popcount order
+    const bool sorted = false;
     nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey, sorted);
     if (p.flags & F_STATS) {
       tdd[0] = td1 - td0;
