@@ -662,6 +662,37 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
   return K;
 }
 
+// Rows reordered by descending popcount (counting sort; order inside a popcount is arbitrary).
+// hist: shared memory with >= 32*W + 1 entries.
+__device__ __noinline__ void popc_sort_rows_desc(const uint32_t* src, uint32_t n, uint32_t W, uint32_t* dst,
+                                                 uint32_t* hist, int lane) {
+  const uint32_t nb = 32 * W + 1;
+  for (uint32_t b = lane; b < nb; b += 32) hist[b] = 0;
+  __syncwarp();
+  for (uint32_t t = lane; t < n; t += 32) {
+    uint32_t pc = 0;
+    for (uint32_t q = 0; q < W; ++q) pc += __popc(src[(size_t)t * W + q]);
+    atomicAdd(&hist[32 * W - pc], 1u);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    uint32_t run = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+      const uint32_t c = hist[b];
+      hist[b] = run;
+      run += c;
+    }
+  }
+  __syncwarp();
+  for (uint32_t t = lane; t < n; t += 32) {
+    uint32_t pc = 0;
+    for (uint32_t q = 0; q < W; ++q) pc += __popc(src[(size_t)t * W + q]);
+    const uint32_t pos = atomicAdd(&hist[32 * W - pc], 1u);
+    for (uint32_t q = 0; q < W; ++q) dst[(size_t)pos * W + q] = src[(size_t)t * W + q];
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ uint32_t antichain_w(uint32_t Wc, const uint32_t* src, uint32_t n, uint32_t* dst,
                                                 bool keep_all, int lane, WarpSmem* sm,
                                                 unsigned long long* kmeta_g = nullptr, bool sorted_desc = false) {
@@ -1122,7 +1153,13 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     // sibling tasks that will read it, keeping the rows unreduced is cheaper (exact either way).
     const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256) ||
                           (qn > p.ac_min && qn > p.ac_ratio * (nPc + 1));
-    const bool sorted = false;
+    bool sorted = false;
+    if (!keep_all && Wc <= 4 && qn > 128) {  // descending popcount: the antichain needs no removal pass
+      uint32_t* tmp = qsrc == w.pbuf ? w.qbuf : w.pbuf;
+      popc_sort_rows_desc(qsrc, qn, Wc, tmp, w.sm->sval, lane);
+      qsrc = tmp;
+      sorted = true;
+    }
     nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey, sorted);
     if (p.flags & F_STATS) {
       tdd[0] = td1 - td0;
