@@ -30,6 +30,12 @@
 #include "mbe_internal.h"
 
 #define FULLMASK 0xffffffffu
+#ifndef MBE_SCAN_MLP
+#define MBE_SCAN_MLP 8  // reverse-scan visits in flight per lane
+#endif
+#ifndef MBE_CLS_MLP
+#define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification
+#endif
 #define KIND_LIST 0u
 #define KIND_BITMAP 1u
 #define TAG_R 0xffffffffu
@@ -930,11 +936,11 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     const uint32_t total = __shfl_sync(FULLMASK, incl, 31);
     visits += total;
     // 4 flattened visits per lane per iteration: independent loads/atomics in flight (MLP)
-    for (uint32_t fb = 0; fb < total; fb += 128) {
-      uint32_t vv[4], pos[4];
-      bool fv[4];
+    for (uint32_t fb = 0; fb < total; fb += 32 * MBE_SCAN_MLP) {
+      uint32_t vv[MBE_SCAN_MLP], pos[MBE_SCAN_MLP];
+      bool fv[MBE_SCAN_MLP];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < MBE_SCAN_MLP; ++j) {
         uint32_t f = fb + 32 * j + lane;
         fv[j] = f < total;
         int lo = 0;
@@ -949,12 +955,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
         pos[j] = base + lo;
         vv[j] = fv[j] ? __ldg(&g.adjV[o_st + (f - (o_incl - o_d))]) : 0u;
       }
-      uint32_t old[4];
+      uint32_t old[MBE_SCAN_MLP];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
+      for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
       if (bm) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < MBE_SCAN_MLP; ++j)
           if (fv[j]) {
             const uint32_t q = pos[j] >> 5;
             uint32_t* wd = q < 4 ? &w.slot[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + q]
@@ -963,7 +969,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
           }
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < MBE_SCAN_MLP; ++j) {
         bool isnew = old[j] == 0u;
         uint32_t b = __ballot_sync(FULLMASK, isnew);
         if (isnew) w.touched[nt + __popc(b & lanemask_lt())] = vv[j];
@@ -980,16 +986,16 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   bool nonmax = false;
   uint32_t nPc = 0, nQc = 0, nRx = 0;
   unsigned long long sRx = 0;
-  for (uint32_t tb = 0; tb < nt; tb += 64) {
-    uint32_t vs[2];
-    uint4 sa[2], sb[2];
+  for (uint32_t tb = 0; tb < nt; tb += 32 * MBE_CLS_MLP) {
+    uint32_t vs[MBE_CLS_MLP];
+    uint4 sa[MBE_CLS_MLP], sb[MBE_CLS_MLP];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < MBE_CLS_MLP; ++j) {
       uint32_t t = tb + 32 * j + lane;
       vs[j] = t < nt ? w.touched[t] : 0xffffffffu;
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < MBE_CLS_MLP; ++j) {
       if (vs[j] != 0xffffffffu) {
         const uint4* sp = reinterpret_cast<const uint4*>(w.slot + (size_t)vs[j] * MBE_SLOT_WORDS);
         sa[j] = sp[0];
@@ -1000,7 +1006,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < MBE_CLS_MLP; ++j) {
       if (vs[j] != 0xffffffffu) {
         uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)vs[j] * MBE_SLOT_WORDS);
         sp[0] = make_uint4(0u, 0u, 0u, 0u);
@@ -1008,7 +1014,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < MBE_CLS_MLP; ++j) {
     const bool valid = vs[j] != 0xffffffffu;
     const uint32_t v = valid ? vs[j] : 0u;
     const uint32_t c = sa[j].x;
