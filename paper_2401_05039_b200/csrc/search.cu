@@ -31,10 +31,10 @@
 
 #define FULLMASK 0xffffffffu
 #ifndef MBE_SCAN_MLP
-#define MBE_SCAN_MLP 8  // reverse-scan visits in flight per lane
+#define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
 #endif
 #ifndef MBE_CLS_MLP
-#define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification
+#define MBE_CLS_MLP 2   // touched-vertex slots in flight per lane during classification
 #endif
 #define KIND_LIST 0u
 #define KIND_BITMAP 1u
