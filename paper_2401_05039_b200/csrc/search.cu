@@ -1342,6 +1342,51 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     nQc += __popc(bq);
   }
   __syncwarp();
+  if (nPc == 1) {
+    // The child frame would hold ONE task: x2 = P'[0] with L'' = row'(x2), Q-role = Q', P-role = ∅
+    // (Algorithm 1 on a one-element P).  Run it inline instead of building/publishing a frame.
+    const uint32_t x2 = (uint32_t)kbuf[0];
+    uint32_t r2[4] = {0u, 0u, 0u, 0u};
+    for (uint32_t q = 0; q < Wn; ++q) r2[q] = pbuf[q];
+    bool dom = false;
+    for (uint32_t cb = 0; cb < nQc; cb += 32) {
+      const uint32_t t = cb + lane;
+      bool sup = t < nQc;
+      for (uint32_t q = 0; q < Wn && sup; ++q) sup = (r2[q] & ~qbuf[(size_t)t * Wn + q]) == 0u;
+      if (__any_sync(FULLMASK, sup)) {
+        dom = true;
+        break;
+      }
+    }
+    account_task(w, p, dom);
+    if (lane == 0 && (p.flags & F_STATS)) {
+      w.bitmap_tasks++;
+      w.alg_bytes += 4ull * Wn * (1ull + nQc);
+    }
+    if (!dom) {
+      unsigned long long sL2 = 0;
+      uint32_t k2 = 0, before = 0;
+      for (uint32_t q = 0; q < Wn; ++q) {
+        const uint32_t wd = r2[q];
+        if ((wd >> lane) & 1u) {
+          const uint32_t id = lbuf[q * 32 + lane];
+          sL2 += g.hvV[id];
+          if (p.cap_records) w.touched[before + __popc(wd & lanemask_lt())] = id;
+        }
+        before += __popc(wd);
+        k2 += __popc(wd);
+      }
+      sL2 = warp_sum64(sL2);
+      account_emit(w, p, sL2, k2, sRp + g.hvU[x2], nRp + 1);
+      if (p.cap_records) {
+        if (lane == 0) rbuf[nRx] = x2;
+        __syncwarp();
+        write_record(w.lane, p, w.touched, k2, R, nR, x, rbuf, nRx + 1);
+      }
+    }
+    MBE_PHASE(14, tph);
+    return;
+  }
   if (smP) sort_pairs_small(kbuf, vbuf, nPc, w.sm, lane);
   else warp_sort_pairs(w, p, nPc, k);
   MBE_PHASE(13, tph);
