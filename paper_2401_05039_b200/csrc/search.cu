@@ -414,11 +414,11 @@ __device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint
         if (row_subset<W>(r, km)) dom = true;
       }
     }
-    uint32_t vb = __ballot_sync(FULLMASK, valid);
-#pragma unroll 4
-    for (int m = 0; m < 32; ++m) {
+    // intra-chunk dominance: only the valid candidates of this chunk (usually a handful)
+    const int nv = (int)min(32u, n - base);
+    for (int m = 0; m < nv; ++m) {
       Row<W> mr = shfl_row<W>(r, m);
-      if (((vb >> m) & 1u) && m != lane && row_subset<W>(r, mr) && (!row_eq<W>(r, mr) || m < lane)) dom = true;
+      if (m != lane && row_subset<W>(r, mr) && (!row_eq<W>(r, mr) || m < lane)) dom = true;
     }
     bool surv = valid && !dom;
     uint32_t bs = __ballot_sync(FULLMASK, surv);
@@ -613,10 +613,10 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
         if (!dom && meta_may_subset(mr, mk) && wide_subset(r, dst + (size_t)(kb + m) * W, W)) dom = true;
       }
     }
-    const uint32_t vb = __ballot_sync(FULLMASK, valid);
-    for (int m = 0; m < 32; ++m) {
+    const int nv = (int)min(32u, n - base);
+    for (int m = 0; m < nv; ++m) {
       const unsigned long long mm = __shfl_sync(FULLMASK, mr, m);
-      if (!dom && ((vb >> m) & 1u) && m != lane && meta_may_subset(mr, mm)) {
+      if (!dom && m != lane && meta_may_subset(mr, mm)) {
         const uint32_t* o = src + (size_t)(base + m) * W;
         if (wide_subset(r, o, W) && (m < lane || !wide_eq(r, o, W))) dom = true;
       }
