@@ -506,7 +506,11 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   }
   const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : 256;
   // persistent kernel: every CTA must be co-resident, so clamp to the occupancy limit
-  const int max_res = mbe_search_max_ctas_per_sm((int)threads, mbe_search_smem_per_warp() * (int)(threads / 32));
+  // instrumented kernel instantiation only when stats / per-root counters / a listing are requested
+  const bool instr = (cfg.flags & MBE_STATS) || cfg.per_root || (out && out->cap_records);
+  const int smem_warp = instr ? mbe_search_smem_per_warp_instr() : mbe_search_smem_per_warp();
+  const int max_res = instr ? mbe_search_max_ctas_per_sm_instr((int)threads, smem_warp * (int)(threads / 32))
+                            : mbe_search_max_ctas_per_sm((int)threads, smem_warp * (int)(threads / 32));
   if (max_res <= 0) return fail(MBE_ECUDA, "occupancy query failed for threads_per_cta=" + std::to_string(threads));
   const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : 2u, (uint32_t)max_res);
   const uint32_t grid = (uint32_t)g->sm_count * ctas_per_sm;
@@ -648,8 +652,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     CUDA_TRY(cudaMemsetAsync(W->tops.p, 0, 4ull * n_warps, st));
     CUDA_TRY(cudaMemsetAsync(W->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
     if (p.per_root) CUDA_TRY(cudaMemsetAsync(W->per_root.p, 0, 32ull * S.nU, st));
-    const int smem = mbe_search_smem_per_warp() * (int)(threads / 32);
-    if (mbe_launch_search(p, (int)grid, (int)threads, smem, st, g->ev0, g->ev1) != 0)
+    const int smem = smem_warp * (int)(threads / 32);
+    const int lrc = instr ? mbe_launch_search_instr(p, (int)grid, (int)threads, smem, st, g->ev0, g->ev1)
+                          : mbe_launch_search(p, (int)grid, (int)threads, smem, st, g->ev0, g->ev1);
+    if (lrc != 0)
       return fail(MBE_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(cudaGetLastError()));
     Globals hg;
     CUDA_TRY(cudaMemcpyAsync(&hg, W->gl.p, sizeof(Globals), cudaMemcpyDeviceToHost, st));

@@ -100,5 +100,9 @@ struct SearchParams {
 // Launches the twin pre-pass and the persistent search kernel on `stream`;
 // ev0/ev1 (cudaEvent_t) bracket the search kernel alone.
 int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1);
+int mbe_launch_search_instr(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0,
+                            void* ev1);
 int mbe_search_smem_per_warp();
 int mbe_search_max_ctas_per_sm(int block, int smem_bytes);
+int mbe_search_smem_per_warp_instr();
+int mbe_search_max_ctas_per_sm_instr(int block, int smem_bytes);

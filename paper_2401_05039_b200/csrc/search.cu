@@ -30,6 +30,23 @@
 #include "mbe_internal.h"
 
 #define FULLMASK 0xffffffffu
+// Two instantiations of this file: the plain search (MBE_INSTR = 0, what runs in benchmarks) has
+// every instrumentation path compiled out, keeping the hot code compact for the instruction cache;
+// search_instr.cu includes it with MBE_INSTR = 1 for MBE_STATS, per-root counters and listings.
+#ifndef MBE_INSTR
+#define MBE_INSTR 0
+#endif
+#if MBE_INSTR
+#define MBE_STATS_ON ((p.flags & F_STATS) != 0)
+#define MBE_PER_ROOT (p.per_root)
+#define MBE_CAP_RECORDS (p.cap_records)
+#define MBE_EXPORT(name) name##_instr
+#else
+#define MBE_STATS_ON (false)
+#define MBE_PER_ROOT ((unsigned long long*)nullptr)
+#define MBE_CAP_RECORDS 0ull
+#define MBE_EXPORT(name) name
+#endif
 #ifndef MBE_SCAN_MLP
 #define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
 #endif
@@ -130,7 +147,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // MBE_STATS sub-phase accounting: add the cycles since `t` to phase k and restart `t`.
 #define MBE_PHASE(k, t)                                              \
   do {                                                               \
-    if ((p.flags & F_STATS) && w.lane == 0) {                        \
+    if (MBE_STATS_ON && w.lane == 0) {                        \
       unsigned long long now_ = (unsigned long long)clock64();       \
       w.sm->ph[k] += now_ - (t);                                     \
       atomicMax(&p.gl->max_phase[k], now_ - (t));                    \
@@ -751,9 +768,9 @@ __device__ __forceinline__ void account_task(Warp& w, const SearchParams& p, boo
   if (w.lane == 0) {
     w.tasks++;
     if (pruned) w.pruned++;
-    if (p.per_root) {
-      atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 2], 1ull);
-      if (pruned) atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 3], 1ull);
+    if (MBE_PER_ROOT) {
+      atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 2], 1ull);
+      if (pruned) atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 3], 1ull);
     }
   }
 }
@@ -764,9 +781,9 @@ __device__ __forceinline__ void account_emit(Warp& w, const SearchParams& p, uin
     uint64_t h = mbe_biclique_hash(p.cand_side, sL, nL, sR, nR);
     w.count++;
     w.hash += h;
-    if (p.per_root) {
-      atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 0], 1ull);
-      atomicAdd(&p.per_root[(size_t)w.cur_root * 4 + 1], (unsigned long long)h);
+    if (MBE_PER_ROOT) {
+      atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 0], 1ull);
+      atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 1], (unsigned long long)h);
     }
   }
 }
@@ -783,7 +800,7 @@ __device__ __noinline__ void write_record(const int lane, const SearchParams& p,
   }
   rec = __shfl_sync(FULLMASK, rec, 0);
   ido = __shfl_sync(FULLMASK, ido, 0);
-  if (rec >= p.cap_records) return;
+  if (rec >= MBE_CAP_RECORDS) return;
   if (ido + nL + nR > p.cap_ids) {
     if (lane == 0) p.rec_off[rec] = ~0ull;  // record counted but its ids did not fit
     return;
@@ -875,11 +892,11 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   // twin pre-pruning at the root (R2 at level 1: an earlier vertex with N(v) = N(x))
   if (root && !(p.flags & F_NO_TWIN) && g.twin[x]) {
     account_task(w, p, true);
-    if (lane == 0 && (p.flags & F_STATS)) w.list_tasks++;
+    if (lane == 0 && MBE_STATS_ON) w.list_tasks++;
     return;
   }
 
-  unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+  unsigned long long tph = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
   const unsigned long long tstart = tph;
   unsigned long long tsub[5] = {0, 0, 0, 0, 0};
   unsigned long long tdd[3] = {0, 0, 0};
@@ -913,7 +930,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     __syncwarp();
   }
 
-  if ((p.flags & F_STATS) && lane == 0) tsub[0] = (unsigned long long)clock64() - tph;
+  if (MBE_STATS_ON && lane == 0) tsub[0] = (unsigned long long)clock64() - tph;
   MBE_PHASE(6, tph);
   // Reverse scan: for u ∈ L' (position pos), for v ∈ N(u): cnt[v]++,
   // bit pos of row(v) when building a bit-row child.  Flattened over the warp.
@@ -980,7 +997,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   sL = warp_sum64(sL);
   __syncwarp();
 
-  if ((p.flags & F_STATS) && lane == 0) tsub[1] = (unsigned long long)clock64() - tph;
+  if (MBE_STATS_ON && lane == 0) tsub[1] = (unsigned long long)clock64() - tph;
   MBE_PHASE(7, tph);
   // Classification of every touched vertex (Steps 3 and 4).
   bool nonmax = false;
@@ -1092,10 +1109,10 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   sRx = warp_sum64(sRx);
   __syncwarp();
 
-  if ((p.flags & F_STATS) && lane == 0) tsub[2] = (unsigned long long)clock64() - tph;
+  if (MBE_STATS_ON && lane == 0) tsub[2] = (unsigned long long)clock64() - tph;
   MBE_PHASE(8, tph);
   account_task(w, p, nonmax);
-  if (lane == 0 && (p.flags & F_STATS)) {
+  if (lane == 0 && MBE_STATS_ON) {
     w.list_tasks++;
     // N(x) + reverse-scan adjacency incl. offsets + touched rows (+ frame L, P, R reads)
     w.alg_bytes += 4ull * dx + 4ull * (visits + nLp) + 8ull * nt + 4ull * (nL + 2ull * nP + nR);
@@ -1105,7 +1122,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   const uint32_t nRp = nR + 1 + nRx;
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, nLp, sRp, nRp);
-  if (p.cap_records) write_record(w.lane, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
+  if (MBE_CAP_RECORDS) write_record(w.lane, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
   if (nPc == 0) return;
 
   // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.  A wide (8/16-word)
@@ -1115,7 +1132,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   const bool cbm = bm && (Wc <= 4 ? (p.narrow_qmax == 0 || nQc <= p.narrow_qmax || nQc <= p.narrow_ratio * nPc)
                                   : (nQc <= p.wide_qcap || (nQc <= p.wide_ratio * nPc && nQc <= p.wide_qmax)));
   warp_sort_pairs(w, p, nPc, nLp);
-  if ((p.flags & F_STATS) && lane == 0) tsub[3] = (unsigned long long)clock64() - tph;
+  if (MBE_STATS_ON && lane == 0) tsub[3] = (unsigned long long)clock64() - tph;
   MBE_PHASE(9, tph);
   const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
                                                             : 2ull * nPc);
@@ -1139,7 +1156,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     __syncwarp();
     const uint32_t* qsrc = w.qbuf;
     uint32_t qn = nQc;
-    const unsigned long long td0 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+    const unsigned long long td0 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
     if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
       // hash table in the (now free) sort-key scratch: 2 x nU u64 entries, power of two >= 2 nQc
       uint32_t lg = 1;
@@ -1152,7 +1169,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       }
       qsrc = w.pbuf;
     }
-    const unsigned long long td1 = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+    const unsigned long long td1 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
     // wide rows with many distinct Q' rows: keep the (exactly deduplicated) rows without the
     // O(n * K) antichain pass; extra dominated rows never change a maximality decision
     // The antichain is one warp's serial O(n * K) pass; when Q' is far larger than the number of
@@ -1167,7 +1184,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       sorted = true;
     }
     nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey, sorted);
-    if (p.flags & F_STATS) {
+    if MBE_STATS_ON {
       tdd[0] = td1 - td0;
       tdd[1] = (unsigned long long)clock64() - td1;
       tdd[2] = qn;
@@ -1186,12 +1203,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
+    if MBE_STATS_ON w.alg_bytes += 4ull * size;
   }
   publish_frame(w, p, size, nPc);
-  if ((p.flags & F_STATS) && lane == 0) tsub[4] = (unsigned long long)clock64() - tph;
+  if (MBE_STATS_ON && lane == 0) tsub[4] = (unsigned long long)clock64() - tph;
   MBE_PHASE(10, tph);
-  if ((p.flags & F_STATS) && lane == 0) {  // diagnostics: remember the longest list task
+  if (MBE_STATS_ON && lane == 0) {  // diagnostics: remember the longest list task
     const unsigned long long dt = (unsigned long long)clock64() - tstart;
     if (atomicMax(&p.gl->longest[0], dt) < dt) {
       unsigned long long* L = p.gl->longest;
@@ -1215,7 +1232,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   const uint32_t* Prow = F + align4((uint64_t)(Pid + nP - F));
   const uint32_t* Qrow = Prow + (size_t)nP * W;
 
-  unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+  unsigned long long tph = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
   const uint32_t x = Pid[i];
   const Row<W> Lx = load_row<W>(Prow + (size_t)i * W);  // L' = row(x) (Step 2)
   uint32_t k = 0;
@@ -1251,7 +1268,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   }
   MBE_PHASE(11, tph);
   account_task(w, p, nonmax);
-  if (lane == 0 && (p.flags & F_STATS)) {
+  if (lane == 0 && MBE_STATS_ON) {
     w.bitmap_tasks++;
     w.alg_bytes += 4ull * W * (1ull + nP + nQ) + 4ull * nP;
   }
@@ -1310,7 +1327,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
 
   MBE_PHASE(12, tph);
   const bool need_child = nPc > 0;
-  if (!need_child && !p.cap_records) return;
+  if (!need_child && !MBE_CAP_RECORDS) return;
 
   // L' ids in ascending order (L is sorted, positions ascending): into lbuf
 #pragma unroll
@@ -1322,7 +1339,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     if (bit) lbuf[before + __popc(b & lanemask_lt())] = L[q * 32 + lane];
   }
   __syncwarp();
-  if (p.cap_records) write_record(w.lane, p, lbuf, k, R, nR, x, rbuf, nRx);
+  if (MBE_CAP_RECORDS) write_record(w.lane, p, lbuf, k, R, nR, x, rbuf, nRx);
   if (!need_child) return;
 
   // Q' candidates: frame Q rows and Q-role siblings P[j<i] meeting L'
@@ -1359,7 +1376,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
       }
     }
     account_task(w, p, dom);
-    if (lane == 0 && (p.flags & F_STATS)) {
+    if (lane == 0 && MBE_STATS_ON) {
       w.bitmap_tasks++;
       w.alg_bytes += 4ull * Wn * (1ull + nQc);
     }
@@ -1371,14 +1388,14 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
         if ((wd >> lane) & 1u) {
           const uint32_t id = lbuf[q * 32 + lane];
           sL2 += g.hvV[id];
-          if (p.cap_records) w.touched[before + __popc(wd & lanemask_lt())] = id;
+          if (MBE_CAP_RECORDS) w.touched[before + __popc(wd & lanemask_lt())] = id;
         }
         before += __popc(wd);
         k2 += __popc(wd);
       }
       sL2 = warp_sum64(sL2);
       account_emit(w, p, sL2, k2, sRp + g.hvU[x2], nRp + 1);
-      if (p.cap_records) {
+      if (MBE_CAP_RECORDS) {
         if (lane == 0) rbuf[nRx] = x2;
         __syncwarp();
         write_record(w.lane, p, w.touched, k2, R, nR, x, rbuf, nRx + 1);
@@ -1425,7 +1442,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
+    if MBE_STATS_ON w.alg_bytes += 4ull * size;
   }
   publish_frame(w, p, size, nPc);
   MBE_PHASE(14, tph);
@@ -1447,7 +1464,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   const uint32_t* Pid = R + nR;
   const uint32_t* Prow = F + align4((uint64_t)(Pid + nP - F));
   const uint32_t* Qrow = Prow + (size_t)nP * W;
-  unsigned long long tph = (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+  unsigned long long tph = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
 
   const uint32_t x = Pid[i];
   uint32_t* lx = w.sm->lx;
@@ -1492,7 +1509,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   }
   MBE_PHASE(11, tph);
   account_task(w, p, nonmax);
-  if (lane == 0 && (p.flags & F_STATS)) {
+  if (lane == 0 && MBE_STATS_ON) {
     w.bitmap_tasks++;
     w.alg_bytes += 4ull * W * (1ull + nP + nQ) + 4ull * nP;
   }
@@ -1546,7 +1563,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   const uint32_t nRp = nR + 1 + nRx;
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, k, sRp, nRp);
-  if (p.cap_records) write_record(w.lane, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
+  if (MBE_CAP_RECORDS) write_record(w.lane, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
   MBE_PHASE(12, tph);
   if (nPc == 0) return;
 
@@ -1610,7 +1627,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if (p.flags & F_STATS) w.alg_bytes += 4ull * size;
+    if MBE_STATS_ON w.alg_bytes += 4ull * size;
   }
   publish_frame(w, p, size, nPc);
   MBE_PHASE(14, tph);
@@ -1669,7 +1686,7 @@ __device__ __forceinline__ uint32_t claim_batch(uint32_t rem) {
 }
 
 __device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p) {
-  return (p.flags & F_STATS) ? (unsigned long long)clock64() : 0ull;
+  return MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
 }
 
 // Idle warp: look for a published frame with unclaimed tasks in the warps
@@ -1849,7 +1866,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
           atomicExch(&dsc->claim, 0ull);
           dsc->done = 0u;
           p.tops[gw] = d;
-          if (p.flags & F_STATS) w.sm->ph[5] += clock64() - t0;
+          if MBE_STATS_ON w.sm->ph[5] += clock64() - t0;
           if (w.sm->fc_depth == (int)d) w.sm->fc_depth = -1;
         }
         w.failed = __shfl_sync(FULLMASK, (int)w.failed, 0);
@@ -1899,12 +1916,12 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         if (lane == 0 && npr) {
           w.tasks += npr;
           w.pruned += npr;
-          if (p.per_root) {
-            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 2], (unsigned long long)npr);
-            atomicAdd(&p.per_root[(size_t)F[5] * 4 + 3], (unsigned long long)npr);
+          if (MBE_PER_ROOT) {
+            atomicAdd(&MBE_PER_ROOT[(size_t)F[5] * 4 + 2], (unsigned long long)npr);
+            atomicAdd(&MBE_PER_ROOT[(size_t)F[5] * 4 + 3], (unsigned long long)npr);
           }
           atomicAdd(&dsc->done, npr);
-          if (p.flags & F_STATS) {
+          if MBE_STATS_ON {
             w.bitmap_tasks += npr;
             const uint32_t nP_ = F[2], nQ_ = F[3];
             w.alg_bytes += (unsigned long long)npr * (4ull * (1ull + nP_ + nQ_) + 4ull * nP_);
@@ -1931,7 +1948,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       pos = __shfl_sync(FULLMASK, pos, 0);
       if (pos >= p.g.n_roots) {
         roots_done = true;
-        if (lane == 0 && (p.flags & F_STATS)) atomicMin(&p.gl->t_roots_out, globaltimer_ns() - t_start);
+        if (lane == 0 && MBE_STATS_ON) atomicMin(&p.gl->t_roots_out, globaltimer_ns() - t_start);
         continue;
       }
       xr = p.g.root_order[pos];
@@ -1959,11 +1976,11 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         rot += 97;
       }
       if (!got) {
-        if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[3] += clock64() - t0;
+        if (lane == 0 && MBE_STATS_ON) w.sm->ph[3] += clock64() - t0;
         unsigned long long t1 = stats_clock(p);
         __nanosleep(backoff);
         if (backoff < 2048) backoff <<= 1;
-        if (lane == 0 && (p.flags & F_STATS)) w.sm->ph[4] += clock64() - t1;
+        if (lane == 0 && MBE_STATS_ON) w.sm->ph[4] += clock64() - t1;
         continue;
       }
       backoff = 64;
@@ -1984,12 +2001,12 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         if (lane == 0) {
           atomicAdd(&dsc->done, tend - ti);  // the victim no longer needs to wait for this range
           w.steals += tend - ti;
-          if (p.flags & F_STATS) w.sm->ph[3] += clock64() - t0;
+          if MBE_STATS_ON w.sm->ph[3] += clock64() - t0;
         }
         publish_frame(w, p, fsz, tend, ti);
         continue;
       }
-      if (lane == 0 && (p.flags & F_STATS)) {
+      if (lane == 0 && MBE_STATS_ON) {
         const unsigned long long now = clock64();
         w.sm->ph[3] += now - t0;
         t0 = now;
@@ -2004,7 +2021,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       if (kind != 2) atomicAdd(&dsc->done, 1u);
       if (kind == 1 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
       if (kind == 3) w.steals++;
-      if (p.flags & F_STATS) {
+      if MBE_STATS_ON {
         const int ph = kind == 2 ? 0 : task_phase(F);
         const unsigned long long dt = clock64() - t0;
         w.sm->ph[ph] += dt;
@@ -2022,7 +2039,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
     atomicAdd(&p.gl->tasks, w.tasks);
     atomicAdd(&p.gl->pruned, w.pruned);
     atomicAdd(&p.gl->steals, w.steals);
-    if (p.flags & F_STATS) {
+    if MBE_STATS_ON {
       atomicAdd(&p.gl->list_tasks, w.list_tasks);
       atomicAdd(&p.gl->bitmap_tasks, w.bitmap_tasks);
       atomicAdd(&p.gl->frames, w.frames);
@@ -2095,10 +2112,10 @@ __global__ void __launch_bounds__(256) mbe_twin_kernel(DevGraph g, uint8_t* twin
 
 }  // namespace
 
-int mbe_search_smem_per_warp() { return (int)sizeof(WarpSmem); }
+int MBE_EXPORT(mbe_search_smem_per_warp)() { return (int)sizeof(WarpSmem); }
 
 // Resident CTAs per SM for a launch shape (the persistent kernel needs every CTA co-resident).
-int mbe_search_max_ctas_per_sm(int block, int smem_bytes) {
+int MBE_EXPORT(mbe_search_max_ctas_per_sm)(int block, int smem_bytes) {
   if (cudaFuncSetAttribute(mbe_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
     return 0;
   int n = 0;
@@ -2106,7 +2123,8 @@ int mbe_search_max_ctas_per_sm(int block, int smem_bytes) {
   return n;
 }
 
-int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1) {
+int MBE_EXPORT(mbe_launch_search)(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0,
+                                   void* ev1) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!(p.flags & F_NO_TWIN)) {
     mbe_twin_kernel<<<148 * 8, 256, 0, s>>>(p.g, const_cast<uint8_t*>(p.g.twin));
