@@ -48,7 +48,7 @@
 #define MBE_EXPORT(name) name
 #endif
 #ifndef MBE_NARROW_TEMPLATES
-#define MBE_NARROW_TEMPLATES 0  // 1: separate register-resident 2- and 4-word task bodies
+#define MBE_NARROW_TEMPLATES 6  // bit mask: 2 / 4 = separate register-resident 2- / 4-word task bodies
 #endif
 #ifndef MBE_SCAN_MLP
 #define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
@@ -1655,15 +1655,14 @@ __device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const u
     const uint32_t W = (h >> 8) & 0xffu;
     // 1-word rows (the bulk of all tasks) have a register-resident specialisation; wider rows
     // share the word-sliced implementation (one copy of the code: instruction-cache footprint)
-#if MBE_NARROW_TEMPLATES
     if (W == 1) bitmap_task<1>(w, p, F, i);
+#if MBE_NARROW_TEMPLATES & 2
     else if (W == 2) bitmap_task<2>(w, p, F, i);
-    else if (W == 4) bitmap_task<4>(w, p, F, i);
-    else bitmap_task_wide(w, p, F, i);
-#else
-    if (W == 1) bitmap_task<1>(w, p, F, i);
-    else bitmap_task_wide(w, p, F, i);
 #endif
+#if MBE_NARROW_TEMPLATES & 4
+    else if (W == 4) bitmap_task<4>(w, p, F, i);
+#endif
+    else bitmap_task_wide(w, p, F, i);
   }
 }
 
