@@ -866,6 +866,120 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
   __syncwarp();
 }
 
+// ================================================================== eager maximality check
+// Step 3 for EVERY task of a freshly built bit-row child frame, run once by the
+// warp that built it (rows still hot in L1/shared memory) instead of once per scheduled task:
+// task t (row r_t, rows in ascending key order) is pruned iff
+//   (a) an earlier sibling has an identical row — with ascending keys only an identical row can
+//       contain r_t (R2), and identical rows share the key block (key = popc(row)), or
+//   (b) some Q row contains r_t.
+// ~93% of all tasks end here, so they are never claimed, cached or dispatched.
+// Writes the surviving task indices (ascending) to S; returns their number.
+template <int W>
+__device__ __forceinline__ bool prune_q_rows(const Row<W>& r, bool alive, const uint32_t* Qr, uint32_t nQ) {
+  for (uint32_t qb = 0; qb < nQ; qb += 8) {
+    if (!__any_sync(FULLMASK, alive)) break;
+    Row<W> s[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] = qb + u < nQ ? load_row<W>(Qr + (size_t)(qb + u) * W) : zero_row<W>();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (qb + u < nQ && row_subset<W>(r, s[u])) alive = false;
+  }
+  return alive;
+}
+
+template <int W>
+__device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, uint32_t nP, const uint32_t* Qr, uint32_t nQ,
+                                             uint32_t* S, int lane) {
+  uint32_t nS = 0;
+  for (uint32_t tb = 0; tb < nP; tb += 32) {
+    const uint32_t t = tb + lane;
+    bool alive = t < nP;
+    const Row<W> r = alive ? load_row<W>(Pr + (size_t)t * W) : zero_row<W>();
+    uint32_t key = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) key += __popc(r.w[q]);
+    for (int j = (int)t - 1; alive && j >= 0; --j) {
+      const Row<W> s = load_row<W>(Pr + (size_t)j * W);
+      uint32_t kj = 0;
+#pragma unroll
+      for (int q = 0; q < W; ++q) kj += __popc(s.w[q]);
+      if (kj != key) break;
+      if (row_eq<W>(r, s)) alive = false;
+    }
+    alive = prune_q_rows<W>(r, alive, Qr, nQ);
+    const uint32_t b = __ballot_sync(FULLMASK, alive);
+    if (alive) S[nS + __popc(b & lanemask_lt())] = t;
+    nS += __popc(b);
+  }
+  __syncwarp();
+  return nS;
+}
+
+// Wide rows (8/16 words): the same test word-sliced, rows read from memory (L1).
+__device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t nP, const uint32_t* Qr, uint32_t nQ,
+                                                  uint32_t W, uint32_t* S, int lane) {
+  uint32_t nS = 0;
+  for (uint32_t tb = 0; tb < nP; tb += 32) {
+    const uint32_t t = tb + lane;
+    bool alive = t < nP;
+    const uint32_t* r = Pr + (size_t)(alive ? t : 0u) * W;
+    uint32_t key = 0;
+    for (uint32_t q = 0; q < W; ++q) key += __popc(r[q]);
+    for (int j = (int)t - 1; alive && j >= 0; --j) {
+      const uint32_t* s = Pr + (size_t)j * W;
+      uint32_t kj = 0, diff = 0;
+      for (uint32_t q = 0; q < W; ++q) {
+        kj += __popc(s[q]);
+        diff |= s[q] ^ r[q];
+      }
+      if (kj != key) break;
+      if (diff == 0u) alive = false;
+    }
+    for (uint32_t qi = 0; qi < nQ; ++qi) {
+      if ((qi & 7u) == 0u && !__any_sync(FULLMASK, alive)) break;
+      if (alive) {
+        const uint32_t* s = Qr + (size_t)qi * W;
+        uint32_t m = 0;
+        for (uint32_t q = 0; q < W && m == 0u; ++q) m |= r[q] & ~s[q];
+        if (m == 0u) alive = false;
+      }
+    }
+    const uint32_t b = __ballot_sync(FULLMASK, alive);
+    if (alive) S[nS + __popc(b & lanemask_lt())] = t;
+    nS += __popc(b);
+  }
+  __syncwarp();
+  return nS;
+}
+
+__device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr, uint32_t nP, const uint32_t* Qr,
+                                                  uint32_t nQ, uint32_t* S, int lane) {
+  __syncwarp();
+  if (W == 1) return prune_frame<1>(Pr, nP, Qr, nQ, S, lane);
+  if (W == 2) return prune_frame<2>(Pr, nP, Qr, nQ, S, lane);
+  if (W == 4) return prune_frame<4>(Pr, nP, Qr, nQ, S, lane);
+  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, lane);
+}
+
+// Account the nP tasks of a child frame decided at build time (nS survive the check).
+__device__ __forceinline__ void account_children(Warp& w, const SearchParams& p, uint32_t nP, uint32_t nS,
+                                                 uint32_t W, uint32_t nQ) {
+  if (w.lane == 0) {
+    w.tasks += nP;
+    w.pruned += nP - nS;
+    if (MBE_PER_ROOT) {
+      atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 2], (unsigned long long)nP);
+      atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 3], (unsigned long long)(nP - nS));
+    }
+    if (MBE_STATS_ON) {
+      w.bitmap_tasks += nP;
+      w.alg_bytes += (unsigned long long)nP * (4ull * W * (1ull + nP + nQ) + 4ull * nP);
+    }
+  }
+}
+
 // ================================================================== list path
 // Task x on a list frame F (or the implicit root frame when F == nullptr:
 // L = V, R = ∅, Q-role = ranks < x, P-role = ranks > x).
@@ -1137,7 +1251,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   warp_sort_pairs(w, p, nPc, nLp);
   if (MBE_STATS_ON && lane == 0) tsub[3] = (unsigned long long)clock64() - tph;
   MBE_PHASE(9, tph);
-  const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (1 + Wc) + (uint64_t)nQc * Wc
+  const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (2 + Wc) + (uint64_t)nQc * Wc
                                                             : 2ull * nPc);
   if (!arena_reserve(w, p, need)) return;
   uint32_t* C = w.arena + w.atop;
@@ -1149,6 +1263,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
   uint64_t size;
   uint32_t nQk = 0;
+  uint32_t nT = nPc;  // tasks published (bit-row children: the survivors of the eager check)
   if (cbm) {
     uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
     for (uint32_t t = lane; t < nPc; t += 32) {
@@ -1192,23 +1307,28 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       tdd[1] = (unsigned long long)clock64() - td1;
       tdd[2] = qn;
     }
-    size = (uint64_t)(CQ + (size_t)nQk * Wc - C);
+    uint32_t* S = CQ + (size_t)nQk * Wc;  // survivor list of the eager check
+    nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, lane);
+    account_children(w, p, nPc, nT, Wc, nQk);
+    size = (uint64_t)(S + nT - C);
   } else {
     uint32_t* CK = CP + nPc;
     for (uint32_t t = lane; t < nPc; t += 32) CK[t] = (uint32_t)(w.skey[t] >> 32);
     size = (uint64_t)(CK + nPc - C);
   }
-  if (lane == 0) {
-    C[0] = (cbm ? KIND_BITMAP : KIND_LIST) | ((cbm ? Wc : 0u) << 8);
-    C[1] = nLp;
-    C[2] = nPc;
-    C[3] = nQk;
-    C[4] = nRp;
-    C[5] = w.cur_root;
-    *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if MBE_STATS_ON w.alg_bytes += 4ull * size;
+  if (nT > 0) {
+    if (lane == 0) {
+      C[0] = (cbm ? KIND_BITMAP : KIND_LIST) | ((cbm ? Wc : 0u) << 8);
+      C[1] = nLp;
+      C[2] = nPc;
+      C[3] = nQk;
+      C[4] = nRp;
+      C[5] = w.cur_root;
+      *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
+      if MBE_STATS_ON w.alg_bytes += 4ull * size;
+    }
+    publish_frame(w, p, size, nT);
   }
-  publish_frame(w, p, size, nPc);
   if (MBE_STATS_ON && lane == 0) tsub[4] = (unsigned long long)clock64() - tph;
   MBE_PHASE(10, tph);
   if (MBE_STATS_ON && lane == 0) {  // diagnostics: remember the longest list task
@@ -1242,40 +1362,9 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
 #pragma unroll
   for (int q = 0; q < W; ++q) k += __popc(Lx.w[q]);
 
-  // Step 3, maximality.  (a) Q-role siblings P[j<i]: with ascending keys only an
-  // identical row can contain L' (R2), and identical rows share the key block.
-  bool nonmax = false;
-  for (uint32_t cb = 0; cb < i; cb += 32) {
-    int j = (int)i - 1 - (int)cb - lane;
-    bool valid = j >= 0;
-    Row<W> r = valid ? load_row<W>(Prow + (size_t)j * W) : zero_row<W>();
-    uint32_t pk = 0;
-#pragma unroll
-    for (int q = 0; q < W; ++q) pk += __popc(r.w[q]);
-    if (__any_sync(FULLMASK, valid && row_eq<W>(r, Lx))) {
-      nonmax = true;
-      break;
-    }
-    if (__any_sync(FULLMASK, !valid || pk < k)) break;
-  }
-  // (b) the frame's Q rows
-  if (!nonmax) {
-    for (uint32_t qb = 0; qb < nQ; qb += 32) {
-      bool valid = qb + lane < nQ;
-      Row<W> r = valid ? load_row<W>(Qrow + (size_t)(qb + lane) * W) : zero_row<W>();
-      if (__any_sync(FULLMASK, valid && row_subset<W>(Lx, r))) {
-        nonmax = true;
-        break;
-      }
-    }
-  }
+  // Step 3 (maximality) was decided for every task of this frame when it was built
+  // (prune_frame): only surviving tasks are ever scheduled, and they were accounted then.
   MBE_PHASE(11, tph);
-  account_task(w, p, nonmax);
-  if (lane == 0 && MBE_STATS_ON) {
-    w.bitmap_tasks++;
-    w.alg_bytes += 4ull * W * (1ull + nP + nQ) + 4ull * nP;
-  }
-  if (nonmax) return;
 
   // Step 4, expansion over P-role rows j > i.
   const uint32_t Wn = mbe_words_for(k);
@@ -1411,7 +1500,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   else warp_sort_pairs(w, p, nPc, k);
   MBE_PHASE(13, tph);
 
-  const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (1 + Wn) + (uint64_t)nQc * Wn;
+  const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (2 + Wn) + (uint64_t)nQc * Wn;
   if (!arena_reserve(w, p, need)) return;
   uint32_t* C = w.arena + w.atop;
   uint32_t* CL = C + MBE_HDR_WORDS;
@@ -1436,7 +1525,14 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   } else {
     nQk = antichain_w(Wn, qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
   }
-  uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
+  uint32_t* S = CQ + (size_t)nQk * Wn;
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, CQ, nQk, S, lane);
+  account_children(w, p, nPc, nS, Wn, nQk);
+  if (nS == 0) {
+    MBE_PHASE(14, tph);
+    return;
+  }
+  uint64_t size = (uint64_t)(S + nS - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
     C[1] = k;
@@ -1447,7 +1543,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
     if MBE_STATS_ON w.alg_bytes += 4ull * size;
   }
-  publish_frame(w, p, size, nPc);
+  publish_frame(w, p, size, nS);
   MBE_PHASE(14, tph);
 }
 
@@ -1475,48 +1571,8 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   __syncwarp();
   const uint32_t k = __reduce_add_sync(FULLMASK, lane < (int)W ? (uint32_t)__popc(lx[lane]) : 0u);
 
-  // Step 3: (a) identical earlier sibling in the equal-key block (R2), (b) Q rows ⊇ row(x)
-  bool nonmax = false;
-  for (uint32_t cb = 0; cb < i; cb += 32) {
-    const int j = (int)i - 1 - (int)cb - lane;
-    const bool valid = j >= 0;
-    bool eq = valid;
-    uint32_t pk = 0;
-    if (valid) {
-      const uint32_t* r = Prow + (size_t)j * W;
-      for (uint32_t q = 0; q < W; ++q) {
-        const uint32_t a = r[q];
-        pk += __popc(a);
-        eq &= a == lx[q];
-      }
-    }
-    if (__any_sync(FULLMASK, eq)) {
-      nonmax = true;
-      break;
-    }
-    if (__any_sync(FULLMASK, !valid || pk < k)) break;
-  }
-  if (!nonmax) {
-    for (uint32_t qb = 0; qb < nQ; qb += 32) {
-      const bool valid = qb + lane < nQ;
-      bool sub = valid;
-      if (valid) {
-        const uint32_t* r = Qrow + (size_t)(qb + lane) * W;
-        for (uint32_t q = 0; q < W && sub; ++q) sub = (lx[q] & ~r[q]) == 0u;
-      }
-      if (__any_sync(FULLMASK, sub)) {
-        nonmax = true;
-        break;
-      }
-    }
-  }
+  // Step 3 was decided when the frame was built (prune_frame_wide): this task is maximal.
   MBE_PHASE(11, tph);
-  account_task(w, p, nonmax);
-  if (lane == 0 && MBE_STATS_ON) {
-    w.bitmap_tasks++;
-    w.alg_bytes += 4ull * W * (1ull + nP + nQ) + 4ull * nP;
-  }
-  if (nonmax) return;
 
   // Step 4: expansion over P-role rows j > i (pbuf keeps the source row index of each P' candidate)
   uint32_t nPc = 0, nRx = 0, nQc = 0;
@@ -1592,7 +1648,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   MBE_PHASE(13, tph);
 
   const uint32_t Wn = mbe_words_for(k);
-  const uint64_t need = MBE_HDR_WORDS + k + nRp + 8 + (uint64_t)nPc * (1 + Wn) + 2ull * nQc * Wn;
+  const uint64_t need = MBE_HDR_WORDS + k + nRp + 8 + (uint64_t)nPc * (2 + Wn) + 2ull * nQc * Wn;
   if (!arena_reserve(w, p, need)) return;
   uint32_t* C = w.arena + w.atop;
   uint32_t* CL = C + MBE_HDR_WORDS;
@@ -1621,7 +1677,14 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   for (uint32_t t = 0; t < nQc; ++t) compress_row(F + w.qbuf[t], scratch + (size_t)t * Wn);
   __syncwarp();
   const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
-  const uint64_t size = (uint64_t)(CQ + (size_t)nQk * Wn - C);
+  uint32_t* S = CQ + (size_t)nQk * Wn;
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, CQ, nQk, S, lane);
+  account_children(w, p, nPc, nS, Wn, nQk);
+  if (nS == 0) {
+    MBE_PHASE(14, tph);
+    return;
+  }
+  const uint64_t size = (uint64_t)(S + nS - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
     C[1] = k;
@@ -1632,7 +1695,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
     if MBE_STATS_ON w.alg_bytes += 4ull * size;
   }
-  publish_frame(w, p, size, nPc);
+  publish_frame(w, p, size, nS);
   MBE_PHASE(14, tph);
 }
 
@@ -1653,6 +1716,8 @@ __device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const u
     list_task(w, p, F, i, 0u);
   } else {
     const uint32_t W = (h >> 8) & 0xffu;
+    // claim index -> row index: the frame's survivor list follows its Q rows
+    i = F[align4((uint64_t)MBE_HDR_WORDS + F[1] + F[4] + F[2]) + (size_t)(F[2] + F[3]) * W + i];
     // 1-word rows (the bulk of all tasks) have a register-resident specialisation; wider rows
     // share the word-sliced implementation (one copy of the code: instruction-cache footprint)
     if (W == 1) bitmap_task<1>(w, p, F, i);
@@ -1664,29 +1729,6 @@ __device__ __forceinline__ void run_task(Warp& w, const SearchParams& p, const u
 #endif
     else bitmap_task_wide(w, p, F, i);
   }
-}
-
-// Maximality check of task i on a 1-word bit-row frame (Step 3): an identical
-// earlier sibling (R2, equal-key block) or a Q row containing row(x) prunes it.
-__device__ __forceinline__ bool w1_pruned(const uint32_t* F, uint32_t i, int lane) {
-  const uint32_t nL = F[1], nP = F[2], nQ = F[3], nR = F[4];
-  const uint32_t* Prow = F + align4((uint64_t)MBE_HDR_WORDS + nL + nR + nP);
-  const uint32_t* Qrow = Prow + nP;
-  const uint32_t lx = Prow[i];
-  const uint32_t k = __popc(lx);
-  for (uint32_t cb = 0; cb < i; cb += 32) {
-    const int j = (int)i - 1 - (int)cb - lane;
-    const bool valid = j >= 0;
-    const uint32_t r = valid ? Prow[j] : 0u;
-    if (__any_sync(FULLMASK, valid && r == lx)) return true;
-    if (__any_sync(FULLMASK, !valid || (uint32_t)__popc(r) < k)) break;
-  }
-  for (uint32_t qb = 0; qb < nQ; qb += 32) {
-    const bool valid = qb + lane < nQ;
-    const uint32_t r = valid ? Qrow[qb + lane] : 0u;
-    if (__any_sync(FULLMASK, valid && (lx & ~r) == 0u)) return true;
-  }
-  return false;
 }
 
 // Owner batch size from the number of tasks not yet claimed by it (an upper bound).
@@ -1903,50 +1945,6 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       }
       ti = i;
       kind = 1;
-      // Fast path: most tasks are 1-word bit-row tasks pruned by the maximality check (SURVEY
-      // fact 8); decide those here with a few shared-memory reads, outside the general task
-      // code, so the hot instruction stream stays small.
-      if (F == w.sm->fcache && F[0] == (KIND_BITMAP | (1u << 8))) {
-        // consume the rest of the claimed batch here while tasks keep getting pruned
-        uint32_t npr = 0;
-        bool maximal = false;
-        for (;;) {
-          if (!w1_pruned(F, i, lane)) {
-            maximal = true;
-            break;
-          }
-          ++npr;
-          uint32_t nx = PEND_NONE;
-          if (lane == 0 && w.sm->bcur[d] < w.sm->bend[d]) nx = w.sm->bcur[d]++;
-          nx = __shfl_sync(FULLMASK, nx, 0);
-          if (nx == PEND_NONE) break;
-          i = nx;
-        }
-        if (lane == 0 && npr) {
-          w.tasks += npr;
-          w.pruned += npr;
-          if (MBE_PER_ROOT) {
-            atomicAdd(&MBE_PER_ROOT[(size_t)F[5] * 4 + 2], (unsigned long long)npr);
-            atomicAdd(&MBE_PER_ROOT[(size_t)F[5] * 4 + 3], (unsigned long long)npr);
-          }
-          atomicAdd(&dsc->done, npr);
-          if MBE_STATS_ON {
-            w.bitmap_tasks += npr;
-            const uint32_t nP_ = F[2], nQ_ = F[3];
-            w.alg_bytes += (unsigned long long)npr * (4ull * (1ull + nP_ + nQ_) + 4ull * nP_);
-            const unsigned long long dt = clock64() - t0;
-            w.sm->ph[2] += dt;
-            w.sm->ph[11] += dt;
-            t0 = clock64();
-          }
-        }
-        if (!maximal) {
-          if (lane == 0 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
-          __syncwarp();
-          continue;
-        }
-        ti = i;  // the maximal task runs through the general path below
-      }
     } else if (!roots_done) {
       // ---- empty stack: next level-1 subtree (coarse-grained task)
       unsigned long long pos = 0;
