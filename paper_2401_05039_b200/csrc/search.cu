@@ -889,19 +889,20 @@ __device__ __forceinline__ bool prune_q_rows(const Row<W>& r, bool alive, const 
   return alive;
 }
 
+// Row t (ascending key order) is Pr[perm[t]] (perm == nullptr: Pr[t]).
 template <int W>
-__device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, uint32_t nP, const uint32_t* Qr, uint32_t nQ,
-                                             uint32_t* S, int lane) {
+__device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t* perm, uint32_t nP, const uint32_t* Qr,
+                                             uint32_t nQ, uint32_t* S, int lane) {
   uint32_t nS = 0;
   for (uint32_t tb = 0; tb < nP; tb += 32) {
     const uint32_t t = tb + lane;
     bool alive = t < nP;
-    const Row<W> r = alive ? load_row<W>(Pr + (size_t)t * W) : zero_row<W>();
+    const Row<W> r = alive ? load_row<W>(Pr + (size_t)(perm ? perm[t] : t) * W) : zero_row<W>();
     uint32_t key = 0;
 #pragma unroll
     for (int q = 0; q < W; ++q) key += __popc(r.w[q]);
     for (int j = (int)t - 1; alive && j >= 0; --j) {
-      const Row<W> s = load_row<W>(Pr + (size_t)j * W);
+      const Row<W> s = load_row<W>(Pr + (size_t)(perm ? perm[j] : (uint32_t)j) * W);
       uint32_t kj = 0;
 #pragma unroll
       for (int q = 0; q < W; ++q) kj += __popc(s.w[q]);
@@ -957,9 +958,9 @@ __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t n
 __device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr, uint32_t nP, const uint32_t* Qr,
                                                   uint32_t nQ, uint32_t* S, int lane) {
   __syncwarp();
-  if (W == 1) return prune_frame<1>(Pr, nP, Qr, nQ, S, lane);
-  if (W == 2) return prune_frame<2>(Pr, nP, Qr, nQ, S, lane);
-  if (W == 4) return prune_frame<4>(Pr, nP, Qr, nQ, S, lane);
+  if (W == 1) return prune_frame<1>(Pr, nullptr, nP, Qr, nQ, S, lane);
+  if (W == 2) return prune_frame<2>(Pr, nullptr, nP, Qr, nQ, S, lane);
+  if (W == 4) return prune_frame<4>(Pr, nullptr, nP, Qr, nQ, S, lane);
   return prune_frame_wide(Pr, nP, Qr, nQ, W, S, lane);
 }
 
@@ -1500,7 +1501,20 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   else warp_sort_pairs(w, p, nPc, k);
   MBE_PHASE(13, tph);
 
-  const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (2 + Wn) + (uint64_t)nQc * Wn;
+  // Eager Step 3 for every child task on the scratch rows (raw Q' candidates decide exactly as
+  // their antichain does), before anything is written: most children end here with no survivor.
+  uint32_t* Stmp = w.touched;
+  __syncwarp();
+  const uint32_t nS = Wn == 1   ? prune_frame<1>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
+                      : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
+                                : prune_frame<4>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane);
+  account_children(w, p, nPc, nS, Wn, nQc);
+  if (nS == 0) {
+    MBE_PHASE(14, tph);
+    return;
+  }
+
+  const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (1 + Wn) + (uint64_t)nQc * Wn + nS;
   if (!arena_reserve(w, p, need)) return;
   uint32_t* C = w.arena + w.atop;
   uint32_t* CL = C + MBE_HDR_WORDS;
@@ -1526,12 +1540,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     nQk = antichain_w(Wn, qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
   }
   uint32_t* S = CQ + (size_t)nQk * Wn;
-  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, CQ, nQk, S, lane);
-  account_children(w, p, nPc, nS, Wn, nQk);
-  if (nS == 0) {
-    MBE_PHASE(14, tph);
-    return;
-  }
+  for (uint32_t t = lane; t < nS; t += 32) S[t] = Stmp[t];
   uint64_t size = (uint64_t)(S + nS - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
@@ -1658,32 +1667,46 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
   for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
   uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
-  // ballot-transposed column compression of one source row into Wn words
-  auto compress_row = [&](const uint32_t* src, uint32_t* dst) {
-    for (uint32_t c = 0; c < Wn; ++c) {
-      const uint32_t pidx = c * 32 + lane;
-      uint32_t bit = 0;
-      if (pidx < k) {
-        const uint32_t pos = w.sm->posv[pidx];
-        bit = (src[pos >> 5] >> (pos & 31)) & 1u;
+  // ballot-transposed column compression of n source rows (word offsets from F given by off(t)) into
+  // Wn words each; 8 rows in flight per step (independent loads), lane u stores row t0 + u's words
+  auto compress_rows = [&](uint32_t n, auto off, uint32_t* dst) {
+    for (uint32_t t0 = 0; t0 < n; t0 += 8) {
+      const uint32_t mine = (lane < 8 && t0 + lane < n) ? off(t0 + lane) : 0u;
+      uint32_t o[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) o[u] = __shfl_sync(FULLMASK, mine, u);
+      for (uint32_t c = 0; c < Wn; ++c) {
+        const uint32_t pidx = c * 32 + lane;
+        const uint32_t pos = pidx < k ? (uint32_t)w.sm->posv[pidx] : 0xffffffffu;
+        uint32_t bits[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          bits[u] = (pos != 0xffffffffu && t0 + u < n) ? (F[o[u] + (pos >> 5)] >> (pos & 31)) & 1u : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t word = __ballot_sync(FULLMASK, bits[u] != 0u);
+          if (lane == u && t0 + u < n) dst[(size_t)(t0 + u) * Wn + c] = word;
+        }
       }
-      const uint32_t word = __ballot_sync(FULLMASK, bit != 0u);
-      if (lane == 0) dst[c] = word;
     }
   };
-  for (uint32_t t = 0; t < nPc; ++t) compress_row(Prow + (size_t)w.pbuf[w.sval[t]] * W, CPr + (size_t)t * Wn);
+  const uint32_t prow_off = (uint32_t)(Prow - F);
+  compress_rows(nPc, [&](uint32_t t) { return prow_off + w.pbuf[w.sval[t]] * W; }, CPr);
   uint32_t* CQ = CPr + (size_t)nPc * Wn;
   uint32_t* scratch = CQ + (size_t)nQc * Wn;  // compressed Q' candidates, reduced into CQ below
-  for (uint32_t t = 0; t < nQc; ++t) compress_row(F + w.qbuf[t], scratch + (size_t)t * Wn);
+  compress_rows(nQc, [&](uint32_t t) { return w.qbuf[t]; }, scratch);
   __syncwarp();
-  const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
-  uint32_t* S = CQ + (size_t)nQk * Wn;
-  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, CQ, nQk, S, lane);
-  account_children(w, p, nPc, nS, Wn, nQk);
+  // eager Step 3 against the raw Q' candidates; the antichain only for frames that survive
+  uint32_t* Stmp = w.touched;
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, lane);
+  account_children(w, p, nPc, nS, Wn, nQc);
   if (nS == 0) {
     MBE_PHASE(14, tph);
     return;
   }
+  const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+  uint32_t* S = CQ + (size_t)nQk * Wn;
+  for (uint32_t t = lane; t < nS; t += 32) S[t] = Stmp[t];
   const uint64_t size = (uint64_t)(S + nS - C);
   if (lane == 0) {
     C[0] = KIND_BITMAP | (Wn << 8);
