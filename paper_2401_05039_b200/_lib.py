@@ -16,7 +16,8 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmbe.so")
+# MBE_LIB_PATH: load an alternative build of the same library (A/B timing of build variants)
+LIB_PATH = os.environ.get("MBE_LIB_PATH") or os.path.join(_HERE, "libmbe.so")
 
 MBE_OK, MBE_EINVAL, MBE_ENOMEM, MBE_ECUDA, MBE_EOVERFLOW, MBE_ERANGE, MBE_EDIST, MBE_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7
 MBE_NO_STEAL, MBE_STATS, MBE_NO_ANTICHAIN, MBE_NO_TWIN, MBE_STEAL_ONE = 0x1, 0x2, 0x4, 0x8, 0x10
