@@ -67,8 +67,8 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t *row_ptr, const uint32
 
 typedef struct {
   uint32_t struct_size;      /* ABI versioning: sizeof(mbe_config) */
-  uint32_t ctas_per_sm;      /* persistent CTAs per SM; 0 = auto */
-  uint32_t threads_per_cta;  /* multiple of 32, <= 1024; 0 = auto */
+  uint32_t ctas_per_sm;      /* persistent CTAs per SM; 0 = auto (6, clamped to the occupancy limit) */
+  uint32_t threads_per_cta;  /* multiple of 32, <= 128 (the kernel's launch bound); 0 = auto (128) */
   uint32_t bitmap_threshold; /* frames with |L| <= this use bit rows (<= 512); 0 = auto (largest that fits) */
   int32_t candidate_side;    /* 0 = auto (smaller side, ties: side 1), 1 = rows, 2 = cols; result-invariant */
   uint32_t flags;            /* MBE_* flags above */
@@ -116,7 +116,7 @@ typedef struct {
    * included): [6] L' construction + role tags (Eq. 1 "B"), [7] reverse scan, [8] maximality check
    * + expansion classification ("C"+"E"), [9] ordering of P' ("A"), [10] child frame build.
    * Sub-phases of bit-row tasks: [11] maximality check, [12] expansion + emit, [13] Q' rows +
-   * ordering, [14] child frame build.  [15] reserved. */
+   * ordering, [14] child frame build.  [15] eager maximality check of a bit-row child (prune_frame). */
   uint64_t phase_cycles[16];
   uint64_t max_task_cycles[3]; /* MBE_STATS: longest single task in cycles: [0] level-1, [1] list, [2] bit-row */
   double roots_out_ms;         /* MBE_STATS: time after launch when the level-1 subtree list ran out */

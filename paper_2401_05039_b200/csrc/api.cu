@@ -486,7 +486,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     cfg = *cfg_in;
   }
   if (cfg.world == 0 || cfg.rank >= cfg.world) return fail(MBE_EINVAL, "rank/world");
-  if (cfg.threads_per_cta % 32 || cfg.threads_per_cta > 256) return fail(MBE_EINVAL, "threads_per_cta must be a multiple of 32 <= 256");
+  if (cfg.threads_per_cta % 32 || cfg.threads_per_cta > MBE_BLOCK)
+    return fail(MBE_EINVAL, "threads_per_cta must be a multiple of 32 <= " + std::to_string(MBE_BLOCK));
   if (cfg.bitmap_threshold > 32 * MBE_WMAX) return fail(MBE_EINVAL, "bitmap_threshold > 512");
   if (cfg.candidate_side < 0 || cfg.candidate_side > 2) return fail(MBE_EINVAL, "candidate_side");
   if (out && (out->cap_records && (!out->rec_off || !out->rec_n1 || !out->rec_n2)))
@@ -504,7 +505,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     if (cfg.per_root) std::memset(cfg.per_root, 0, 32ull * S.nU);
     return MBE_OK;
   }
-  const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : 256;
+  const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : MBE_BLOCK;
   // persistent kernel: every CTA must be co-resident, so clamp to the occupancy limit
   // instrumented kernel instantiation only when stats / per-root counters / a listing are requested
   const bool instr = (cfg.flags & MBE_STATS) || cfg.per_root || (out && out->cap_records);
@@ -512,14 +513,14 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   const int max_res = instr ? mbe_search_max_ctas_per_sm_instr((int)threads, smem_warp * (int)(threads / 32))
                             : mbe_search_max_ctas_per_sm((int)threads, smem_warp * (int)(threads / 32));
   if (max_res <= 0) return fail(MBE_ECUDA, "occupancy query failed for threads_per_cta=" + std::to_string(threads));
-  const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : 2u, (uint32_t)max_res);
+  const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : (uint32_t)MBE_MINBLOCKS, (uint32_t)max_res);
   const uint32_t grid = (uint32_t)g->sm_count * ctas_per_sm;
   const uint32_t n_warps = grid * (threads / 32);
   // auto arena: proportional to the graph, 256 KiB .. 8 MiB per warp; grown x4 and retried on overflow
   uint64_t arena = cfg.arena_bytes ? cfg.arena_bytes
                                    : std::min<uint64_t>(8ull << 20, std::max<uint64_t>(256ull << 10, 16ull * (S.nU + S.nV + g->nE)));
   arena = (arena + 255) & ~255ull;
-  // auto bit-row threshold: the widest rows (512 columns) whose workspace fits in 60% of free memory
+  // auto bit-row threshold: the widest rows (512 columns) whose workspace fits in 80% of free memory
   uint32_t T = cfg.bitmap_threshold;
   if (!T) {
     size_t fr = 0, tot = 0;
@@ -532,7 +533,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     }
     T = 128;
     for (uint32_t t : {512u, 256u}) {
-      if ((double)workspace_stride(S.nU, S.maxdegU, arena, mbe_words_for(t)) * n_warps <= 0.6 * (double)(fr + pooled)) {
+      if ((double)workspace_stride(S.nU, S.maxdegU, arena, mbe_words_for(t)) * n_warps <= 0.8 * (double)(fr + pooled)) {
         T = t;
         break;
       }
@@ -569,12 +570,19 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       checkin_workspace(wg.w);
       wg.w = nullptr;
     }
+    const auto tw0 = std::chrono::steady_clock::now();
     if (!wg.w) {
       rc = checkout_workspace(g->device, n_warps, S.nU, S.maxdegU, arena, wmax, &wg.w);
       if (rc) return rc;
     }
     Workspace* W = wg.w;
     if (W->dirty && (rc = clear_tables(W, st))) return rc;
+    if (std::getenv("MBE_DEBUG_TIMING")) {
+      cudaStreamSynchronize(st);
+      std::fprintf(stderr, "  enumerate: workspace checkout + clear %.2f ms (n_warps %u, T %u, arena %llu B, %.1f GB)\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count(), n_warps,
+                   T, (unsigned long long)arena, W->ws.bytes / 1e9);
+    }
     SearchParams& p = g->sp;
     p.g.nU = S.nU;
     p.g.nV = S.nV;
@@ -609,6 +617,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       p.ac_ratio = ar ? (uint32_t)std::strtoul(ar, nullptr, 10) : 0xffffffffu;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
       p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 512u;
+      const char* wa = std::getenv("MBE_WIDE_ACMAX");
+      p.wide_acmax = wa ? (uint32_t)std::strtoul(wa, nullptr, 10) : 256u;
     }
     p.flags = cfg.flags;
     p.rank = cfg.rank;
@@ -698,6 +708,32 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
                    L[0] / 1.965e6, L[1], L[2], L[3], L[4], L[5], L[6], L[7], L[8], L[14], L[15], L[9] / 1.965e6,
                    L[10] / 1.965e6, L[11] / 1.965e6, L[12] / 1.965e6, L[13] / 1.965e6, L[16] / 1.965e6, L[18],
                    L[17] / 1.965e6);
+    }
+    if (std::getenv("MBE_DEBUG_HIST") && (cfg.flags & MBE_STATS)) {
+      for (int b = 0; b < 24; ++b)
+        if (hg.hist[0][b])
+          std::fprintf(stderr, "bit-row tasks |P|+|Q| in [%d,%d): %llu tasks, %.3f ms warp time, %.2f us/task\n",
+                       (1 << b) - 1, (2 << b) - 1, hg.hist[0][b], hg.hist[1][b] / 1.965e6,
+                       hg.hist[1][b] / 1.965e3 / (double)hg.hist[0][b]);
+      std::fprintf(stderr, "warps first idle / exiting per 2 ms:");
+      for (int b = 0; b < 64; ++b)
+        if (hg.busy_hist[b] || hg.exit_hist[b]) std::fprintf(stderr, " [%d] %llu/%llu", 2 * b, hg.busy_hist[b], hg.exit_hist[b]);
+      std::fprintf(stderr, "\n");
+      for (int k = 0; k < 3; ++k) {
+        std::fprintf(stderr, "%s task warp-ms by completion time (2 ms buckets):", k == 0 ? "root" : (k == 1 ? "list" : "bitrow"));
+        for (int b = 0; b < 64; ++b)
+          if (hg.tl_hist[k][b]) std::fprintf(stderr, " [%d] %.0f", 2 * b, hg.tl_hist[k][b] / 1.965e6);
+        std::fprintf(stderr, "\n");
+      }
+      const char* sub[3] = {"compress", "prune", "antichain"};
+      for (int b = 29; b < 32; ++b)
+        if (hg.hist[0][b])
+          std::fprintf(stderr, "wide child build, %s: %llu calls, %.3f ms warp time, %.2f us/call\n", sub[b - 29],
+                       hg.hist[0][b], hg.hist[1][b] / 1.965e6, hg.hist[1][b] / 1.965e3 / (double)hg.hist[0][b]);
+      for (int b = 24; b < 29; ++b)
+        if (hg.hist[0][b])
+          std::fprintf(stderr, "bit-row tasks W=%d: %llu tasks, %.3f ms warp time, %.2f us/task\n", 1 << (b - 24),
+                       hg.hist[0][b], hg.hist[1][b] / 1.965e6, hg.hist[1][b] / 1.965e3 / (double)hg.hist[0][b]);
     }
     res->roots_out_ms = hg.t_roots_out == ~0ull ? -1.0 : (double)hg.t_roots_out * 1e-6;
     if (cfg.per_root) {

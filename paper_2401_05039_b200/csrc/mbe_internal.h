@@ -9,6 +9,14 @@
 #define MBE_SEXT_WORDS 12  // per-vertex extension: bit row words 4-15 (wide rows only)
 #define MBE_SMEM_SORT 256  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
 #define MBE_HDR_WORDS 8    // frame header
+// Persistent launch shape: 128-thread CTAs, 6 per SM (85 registers/thread, 24 warps/SM: more
+// warps in flight beat fewer spills on this latency-bound search).
+#ifndef MBE_BLOCK
+#define MBE_BLOCK 128
+#endif
+#ifndef MBE_MINBLOCKS
+#define MBE_MINBLOCKS 6
+#endif
 
 // Immutable device graph after ingest.  Candidate side U is
 // relabelled by ascending (degree, original id): internal id = rank r(v).
@@ -53,6 +61,11 @@ struct Globals {
   unsigned long long t_roots_out;  // MBE_STATS: ns after launch when the level-1 list ran out
   unsigned long long max_phase[16];  // MBE_STATS: longest single occurrence of each sub-phase (cycles)
   unsigned long long longest[20];    // MBE_STATS diagnostics: the longest list-path task (see search.cu)
+  unsigned long long hist[2][32];    // MBE_STATS diagnostics: bit-row tasks by log2(|P|+|Q|) of their frame [0, 24) and by
+                                     // log2(W) [24, 29): count, cycles
+  unsigned long long exit_hist[64];  // MBE_STATS diagnostics: warps by exit time (2 ms buckets after launch)
+  unsigned long long tl_hist[3][64];  // MBE_STATS diagnostics: task cycles by completion time (2 ms buckets): root, list, bit-row
+  unsigned long long busy_hist[64];  // MBE_STATS diagnostics: warps registering idle for the first time, by time
 };
 
 struct SearchParams {
@@ -64,6 +77,7 @@ struct SearchParams {
   uint32_t wide_qmax;
   uint32_t narrow_qmax, narrow_ratio;  // same guard for 1/2/4-word children (narrow_qmax 0 = always)
   uint32_t dedup_min;
+  uint32_t wide_acmax;  // wide (8/16-word) list-path children keep more distinct Q' rows than this unreduced
   uint32_t ac_min, ac_ratio;  // list-path children skip the antichain if |Q'| > ac_min and > ac_ratio*(|P'|+1)   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;
   uint32_t rank, world;

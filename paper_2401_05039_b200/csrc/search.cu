@@ -248,13 +248,28 @@ __device__ __forceinline__ bool row_any_and(const Row<W>& a, const Row<W>& b) {
 
 // ------------------------------------------------------------------ sorting
 // Ascending sort of n (key, val) pairs in place (keys unique: (count << 32) | id).
+#ifndef MBE_AC_ROLL
+#define MBE_AC_ROLL 1
+#endif
+#ifndef MBE_SORT_ROLLED
+#define MBE_SORT_ROLLED 0
+#endif
 __device__ __noinline__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, int lane) {
   unsigned long long k = lane < (int)n ? key[lane] : ~0ull;
   uint32_t v = lane < (int)n ? val[lane] : 0u;
+#if MBE_SORT_ROLLED
+  // rolled bitonic network over the next power of two >= n (instruction-cache footprint)
+  const int N = n <= 2 ? 2 : 1 << (32 - __clz((int)n - 1));
+#pragma unroll 1
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll 1
+    for (int j = size >> 1; j > 0; j >>= 1) {
+#else
 #pragma unroll
   for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
     for (int j = size >> 1; j > 0; j >>= 1) {
+#endif
       unsigned long long ok = __shfl_xor_sync(FULLMASK, k, j);
       uint32_t ov = __shfl_xor_sync(FULLMASK, v, j);
       bool up = (lane & size) == 0;
@@ -429,6 +444,9 @@ __device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint
       const bool kval = kb + lane < K;
       const Row<W> kr = kval ? load_row<W>(dst + (size_t)(kb + lane) * W) : zero_row<W>();
       const uint32_t nk = min(32u, K - kb);
+#if MBE_AC_ROLL
+#pragma unroll 1
+#endif
       for (uint32_t m = 0; m < nk; ++m) {
         const Row<W> km = shfl_row<W>(kr, (int)m);
         if (row_subset<W>(r, km)) dom = true;
@@ -436,6 +454,9 @@ __device__ __noinline__ uint32_t antichain(const uint32_t* src, uint32_t n, uint
     }
     // intra-chunk dominance: only the valid candidates of this chunk (usually a handful)
     const int nv = (int)min(32u, n - base);
+#if MBE_AC_ROLL
+#pragma unroll 1
+#endif
     for (int m = 0; m < nv; ++m) {
       Row<W> mr = shfl_row<W>(r, m);
       if (m != lane && row_subset<W>(r, mr) && (!row_eq<W>(r, mr) || m < lane)) dom = true;
@@ -628,12 +649,18 @@ __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n,
           kk < K ? (kk < MBE_SMEM_SORT ? kmeta[kk] : (kmeta_g ? kmeta_g[kk] : wide_meta(dst + (size_t)kk * W, W)))
                  : ~0ull;
       const uint32_t nk = min(32u, K - kb);
+#if MBE_AC_ROLL
+#pragma unroll 1
+#endif
       for (uint32_t m = 0; m < nk; ++m) {
         const unsigned long long mk = __shfl_sync(FULLMASK, mkl, (int)m);
         if (!dom && meta_may_subset(mr, mk) && wide_subset(r, dst + (size_t)(kb + m) * W, W)) dom = true;
       }
     }
     const int nv = (int)min(32u, n - base);
+#if MBE_AC_ROLL
+#pragma unroll 1
+#endif
     for (int m = 0; m < nv; ++m) {
       const unsigned long long mm = __shfl_sync(FULLMASK, mr, m);
       if (!dom && m != lane && meta_may_subset(mr, mm)) {
@@ -866,6 +893,69 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
   __syncwarp();
 }
 
+// ================================================================== wide column compression
+// Child rows of a wide (4/8/16-word) task are its parent rows restricted to the set bits of
+// L' = row(x) and packed (column compression, bit gather).  One row per LANE: the lane loads its
+// row's W words and gathers each with the word's precomputed parallel-suffix masks (bits.cuh),
+// streaming the packed bits into Wn output words.  cm (shared memory): [5q + i] = mask i of
+// word q, [80 + q] = output bit offset of word q; lx = row(x).
+__device__ __noinline__ void compress_rows_lanes(const uint32_t* F, const uint32_t* offs, uint32_t n, uint32_t W,
+                                                 const uint32_t* lx, const uint32_t* cm, uint32_t Wn, uint32_t* dst,
+                                                 int lane) {
+  for (uint32_t tb = 0; tb < n; tb += 32) {
+    const uint32_t t = tb + lane;
+    if (t < n) {
+      const uint32_t* src = F + offs[t];
+      uint32_t* out = dst + (size_t)t * Wn;
+      uint32_t acc = 0, accw = 0;
+#pragma unroll 4
+      for (uint32_t q = 0; q < W; ++q) {
+        const uint32_t m = lx[q];
+        uint32_t y = src[q] & m;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const uint32_t tt = y & cm[5 * q + i];
+          y = (y ^ tt) | (tt >> (1 << i));
+        }
+        const uint32_t o = cm[80 + q], d = o >> 5, r = o & 31u;
+        if (d > accw) {  // the previous output word is complete
+          out[accw] = acc;
+          acc = 0;
+          accw = d;
+        }
+        acc |= y << r;
+        if (r != 0u && r + __popc(m) > 32u) {  // spills into the next output word
+          out[accw] = acc;
+          acc = y >> (32u - r);
+          ++accw;
+        }
+      }
+      if (accw < Wn) out[accw++] = acc;
+      for (; accw < Wn; ++accw) out[accw] = 0u;
+    }
+  }
+  __syncwarp();
+}
+
+// Prepare cm for compress_rows_lanes from row(x) = lx[0..W).
+__device__ __forceinline__ void compress_prep_lanes(const uint32_t* lx, uint32_t W, uint32_t* cm, int lane) {
+  const uint32_t m = lane < (int)W ? lx[lane] : 0u;
+  const uint32_t pc = __popc(m);
+  uint32_t incl = pc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULLMASK, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane < (int)W) {
+    const MbeCompress32 c = mbe_compress_prep(m);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) cm[5 * lane + i] = c.mv[i];
+    cm[80 + lane] = incl - pc;
+  }
+  __syncwarp();
+}
+
 // ================================================================== eager maximality check
 // Step 3 for EVERY task of a freshly built bit-row child frame, run once by the
 // warp that built it (rows still hot in L1/shared memory) instead of once per scheduled task:
@@ -918,34 +1008,36 @@ __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t*
   return nS;
 }
 
-// Wide rows (8/16 words): the same test word-sliced, rows read from memory (L1).
+// Wide rows (8/16 words): the same test word-sliced, rows read from memory (L1).  Every row's
+// (popcount, OR-fold) metadata is computed once into `meta` (global scratch, >= nP + nQ entries);
+// its necessary conditions for == and ⊆ filter the pairs, 8 Q rows in flight per step.
 __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t nP, const uint32_t* Qr, uint32_t nQ,
-                                                  uint32_t W, uint32_t* S, int lane) {
+                                                  uint32_t W, uint32_t* S, unsigned long long* meta, int lane) {
+  for (uint32_t t = lane; t < nP + nQ; t += 32)
+    meta[t] = wide_meta(t < nP ? Pr + (size_t)t * W : Qr + (size_t)(t - nP) * W, W);
+  __syncwarp();
+  const unsigned long long* mq = meta + nP;
   uint32_t nS = 0;
   for (uint32_t tb = 0; tb < nP; tb += 32) {
     const uint32_t t = tb + lane;
     bool alive = t < nP;
     const uint32_t* r = Pr + (size_t)(alive ? t : 0u) * W;
-    uint32_t key = 0;
-    for (uint32_t q = 0; q < W; ++q) key += __popc(r[q]);
+    const unsigned long long mr = alive ? meta[t] : 0ull;
+    const uint32_t key = (uint32_t)(mr >> 32);
     for (int j = (int)t - 1; alive && j >= 0; --j) {
-      const uint32_t* s = Pr + (size_t)j * W;
-      uint32_t kj = 0, diff = 0;
-      for (uint32_t q = 0; q < W; ++q) {
-        kj += __popc(s[q]);
-        diff |= s[q] ^ r[q];
-      }
-      if (kj != key) break;
-      if (diff == 0u) alive = false;
+      const unsigned long long mj = meta[j];
+      if ((uint32_t)(mj >> 32) != key) break;
+      if (mj == mr && wide_eq(r, Pr + (size_t)j * W, W)) alive = false;
     }
-    for (uint32_t qi = 0; qi < nQ; ++qi) {
-      if ((qi & 7u) == 0u && !__any_sync(FULLMASK, alive)) break;
-      if (alive) {
-        const uint32_t* s = Qr + (size_t)qi * W;
-        uint32_t m = 0;
-        for (uint32_t q = 0; q < W && m == 0u; ++q) m |= r[q] & ~s[q];
-        if (m == 0u) alive = false;
-      }
+    for (uint32_t qb = 0; qb < nQ; qb += 8) {
+      if (!__any_sync(FULLMASK, alive)) break;
+      unsigned long long m8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m8[u] = qb + u < nQ ? mq[qb + u] : ~0ull;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (alive && qb + u < nQ && meta_may_subset(mr, m8[u]) && wide_subset(r, Qr + (size_t)(qb + u) * W, W))
+          alive = false;
     }
     const uint32_t b = __ballot_sync(FULLMASK, alive);
     if (alive) S[nS + __popc(b & lanemask_lt())] = t;
@@ -956,12 +1048,12 @@ __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t n
 }
 
 __device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr, uint32_t nP, const uint32_t* Qr,
-                                                  uint32_t nQ, uint32_t* S, int lane) {
+                                                  uint32_t nQ, uint32_t* S, unsigned long long* meta, int lane) {
   __syncwarp();
   if (W == 1) return prune_frame<1>(Pr, nullptr, nP, Qr, nQ, S, lane);
   if (W == 2) return prune_frame<2>(Pr, nullptr, nP, Qr, nQ, S, lane);
   if (W == 4) return prune_frame<4>(Pr, nullptr, nP, Qr, nQ, S, lane);
-  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, lane);
+  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, meta, lane);
 }
 
 // Account the nP tasks of a child frame decided at build time (nS survive the check).
@@ -1293,7 +1385,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     // O(n * K) antichain pass; extra dominated rows never change a maximality decision
     // The antichain is one warp's serial O(n * K) pass; when Q' is far larger than the number of
     // sibling tasks that will read it, keeping the rows unreduced is cheaper (exact either way).
-    const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > 256) ||
+    const bool keep_all = (p.flags & F_NO_ANTICHAIN) != 0 || (Wc >= 8 && qn > p.wide_acmax) ||
                           (qn > p.ac_min && qn > p.ac_ratio * (nPc + 1));
     bool sorted = false;
     if (!keep_all && Wc <= 4 && qn > 128) {  // descending popcount: the antichain needs no removal pass
@@ -1309,7 +1401,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       tdd[2] = qn;
     }
     uint32_t* S = CQ + (size_t)nQk * Wc;  // survivor list of the eager check
-    nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, lane);
+    nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, lane);
     account_children(w, p, nPc, nT, Wc, nQk);
     size = (uint64_t)(S + nT - C);
   } else {
@@ -1508,6 +1600,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   const uint32_t nS = Wn == 1   ? prune_frame<1>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
                       : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
                                 : prune_frame<4>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane);
+  MBE_PHASE(15, tph);
   account_children(w, p, nPc, nS, Wn, nQc);
   if (nS == 0) {
     MBE_PHASE(14, tph);
@@ -1560,7 +1653,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
 // Frames with 128 < |L| <= 512 (8 or 16 words per row).  Same steps as
 // bitmap_task, word-sliced: row(x) lives in shared memory, every other row is
 // streamed from memory (L1) one word at a time, and child rows are column-
-// compressed by ballot transposition (lane l gathers column posv[32c + l]).
+// compressed one row per lane (compress_rows_lanes).
 __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p, const uint32_t* F, uint32_t i) {
   const DevGraph& g = p.g;
   const int lane = w.lane;
@@ -1622,7 +1715,6 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
       const uint32_t id = L[q * 32 + lane];
       sL += g.hvV[id];
       w.lbuf[rank] = id;
-      w.sm->posv[rank] = (unsigned short)(q * 32 + lane);
     }
     before += __popc(word);
   }
@@ -1655,6 +1747,15 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   __syncwarp();
   warp_sort_pairs(w, p, nPc, k);
   MBE_PHASE(13, tph);
+  unsigned long long twd = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
+  auto wide_sub = [&](int slot) {  // MBE_STATS diagnostics: wide child-build sub-phases
+    if (MBE_STATS_ON && lane == 0) {
+      const unsigned long long now = (unsigned long long)clock64();
+      atomicAdd(&p.gl->hist[0][slot], 1ull);
+      atomicAdd(&p.gl->hist[1][slot], now - twd);
+      twd = now;
+    }
+  };
 
   const uint32_t Wn = mbe_words_for(k);
   const uint64_t need = MBE_HDR_WORDS + k + nRp + 8 + (uint64_t)nPc * (2 + Wn) + 2ull * nQc * Wn;
@@ -1667,44 +1768,30 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
   for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
   uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
-  // ballot-transposed column compression of n source rows (word offsets from F given by off(t)) into
-  // Wn words each; 8 rows in flight per step (independent loads), lane u stores row t0 + u's words
-  auto compress_rows = [&](uint32_t n, auto off, uint32_t* dst) {
-    for (uint32_t t0 = 0; t0 < n; t0 += 8) {
-      const uint32_t mine = (lane < 8 && t0 + lane < n) ? off(t0 + lane) : 0u;
-      uint32_t o[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) o[u] = __shfl_sync(FULLMASK, mine, u);
-      for (uint32_t c = 0; c < Wn; ++c) {
-        const uint32_t pidx = c * 32 + lane;
-        const uint32_t pos = pidx < k ? (uint32_t)w.sm->posv[pidx] : 0xffffffffu;
-        uint32_t bits[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          bits[u] = (pos != 0xffffffffu && t0 + u < n) ? (F[o[u] + (pos >> 5)] >> (pos & 31)) & 1u : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t word = __ballot_sync(FULLMASK, bits[u] != 0u);
-          if (lane == u && t0 + u < n) dst[(size_t)(t0 + u) * Wn + c] = word;
-        }
-      }
-    }
-  };
+  uint32_t* cm = reinterpret_cast<uint32_t*>(w.sm->posv);  // compression masks (posv is free here)
+  compress_prep_lanes(lx, W, cm, lane);
   const uint32_t prow_off = (uint32_t)(Prow - F);
-  compress_rows(nPc, [&](uint32_t t) { return prow_off + w.pbuf[w.sval[t]] * W; }, CPr);
+  for (uint32_t t = lane; t < nPc; t += 32) w.touched[t] = prow_off + w.pbuf[w.sval[t]] * W;
+  __syncwarp();
+  compress_rows_lanes(F, w.touched, nPc, W, lx, cm, Wn, CPr, lane);
   uint32_t* CQ = CPr + (size_t)nPc * Wn;
   uint32_t* scratch = CQ + (size_t)nQc * Wn;  // compressed Q' candidates, reduced into CQ below
-  compress_rows(nQc, [&](uint32_t t) { return w.qbuf[t]; }, scratch);
+  compress_rows_lanes(F, w.qbuf, nQc, W, lx, cm, Wn, scratch, lane);
   __syncwarp();
   // eager Step 3 against the raw Q' candidates; the antichain only for frames that survive
   uint32_t* Stmp = w.touched;
-  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, lane);
+  MBE_PHASE(14, tph);
+  wide_sub(29);
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, lane);
+  MBE_PHASE(15, tph);
+  wide_sub(30);
   account_children(w, p, nPc, nS, Wn, nQc);
   if (nS == 0) {
     MBE_PHASE(14, tph);
     return;
   }
   const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+  wide_sub(31);
   uint32_t* S = CQ + (size_t)nQk * Wn;
   for (uint32_t t = lane; t < nS; t += 32) S[t] = Stmp[t];
   const uint64_t size = (uint64_t)(S + nS - C);
@@ -1841,10 +1928,7 @@ __device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const 
 }
 
 // ================================================================== kernel
-#ifndef MBE_MINBLOCKS
-#define MBE_MINBLOCKS 2
-#endif
-__global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchParams p) {
+__global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(SearchParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const uint32_t wib = threadIdx.x >> 5;
@@ -1886,6 +1970,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
   const unsigned long long t_start = globaltimer_ns();
   bool roots_done = false;
   bool registered = false;
+  bool ever_idle = false;
   uint32_t backoff = 64;
   uint32_t rot = 0;
 
@@ -1987,6 +2072,9 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
       // ---- idle: register, then steal single tasks or terminate
       if (!registered) {
         if (lane == 0) atomicAdd(&p.gl->idle, 1u);
+        if (lane == 0 && MBE_STATS_ON && !ever_idle)
+          atomicAdd(&p.gl->busy_hist[min(63ull, (globaltimer_ns() - t_start) / 2000000ull)], 1ull);
+        ever_idle = true;
         registered = true;
       }
       uint32_t stop = 0;
@@ -2056,6 +2144,15 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
         const unsigned long long dt = clock64() - t0;
         w.sm->ph[ph] += dt;
         atomicMax(&p.gl->max_task[ph], dt);
+        atomicAdd(&p.gl->tl_hist[ph][min(63ull, (globaltimer_ns() - t_start) / 2000000ull)], dt);
+        if (ph == 2) {
+          const uint32_t b = 31u - __clz(F[2] + F[3] + 1u);
+          atomicAdd(&p.gl->hist[0][b], 1ull);
+          atomicAdd(&p.gl->hist[1][b], dt);
+          const uint32_t bw = 24u + (31u - __clz((F[0] >> 8) & 0xffu));
+          atomicAdd(&p.gl->hist[0][bw], 1ull);
+          atomicAdd(&p.gl->hist[1][bw], dt);
+        }
       }
     }
     __syncwarp();
@@ -2063,6 +2160,7 @@ __global__ void __launch_bounds__(256, MBE_MINBLOCKS) mbe_search_kernel(SearchPa
 
   // flush lane-0 accumulators
   if (lane == 0) {
+    if MBE_STATS_ON atomicAdd(&p.gl->exit_hist[min(63ull, (globaltimer_ns() - t_start) / 2000000ull)], 1ull);
     p.stamps[gw] = w.stamp;
     atomicAdd(&p.gl->count, w.count);
     atomicAdd(&p.gl->hash, w.hash);

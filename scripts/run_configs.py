@@ -44,10 +44,10 @@ def main():
                               bitmap_tasks=st.bitmap_tasks, frames=st.frames, alg_bytes=st.alg_bytes,
                               max_depth=st.max_depth, stats_kernel_ms=st.kernel_ms,
                               phase_frac_of_warp_time=[round(c / (st.n_warps * st.kernel_ms * 1.965e6), 4)
-                                                       for c in st.phase_cycles[:15]],
+                                                       for c in st.phase_cycles[:16]],
                               max_task_ms=[round(c / 1.965e6, 3) for c in st.max_task_cycles],
                               roots_out_ms=round(st.roots_out_ms, 3),
-                              max_phase_ms=[round(c / 1.965e6, 3) for c in st.max_phase_cycles[:15]],
+                              max_phase_ms=[round(c / 1.965e6, 3) for c in st.max_phase_cycles[:16]],
                               bicliques_per_s=r.count / (min(times) / 1e3))), flush=True)
         G.close()
 

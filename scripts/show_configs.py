@@ -3,7 +3,7 @@ import json
 import sys
 
 NAMES = ["root", "list", "bitrow", "steal", "idle", "popwait", "Lp", "rscan", "cls", "order", "lbuild", "chk", "exp",
-         "Qord", "cbuild", "r"]
+         "Qord", "cbuild", "prune"]
 for f in sys.argv[1:]:
     print("==", f)
     for line in open(f):

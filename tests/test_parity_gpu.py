@@ -116,7 +116,7 @@ def test_wide_bit_rows(g, T):
     assert same(gpu(g, bitmap_threshold=T, flags=MBE_NO_ANTICHAIN), want)
 
 
-@pytest.mark.parametrize("ctas,threads", [(1, 32), (1, 256), (2, 128), (4, 64)])
+@pytest.mark.parametrize("ctas,threads", [(1, 32), (1, 128), (2, 128), (4, 64)])
 def test_launch_shapes(ctas, threads):
     g = I.random_bipartite(200, 150, 0.06, 5)
     assert same(gpu(g, ctas_per_sm=ctas, threads_per_cta=threads), oracle.mbea(g))
@@ -126,7 +126,7 @@ def test_launch_shapes(ctas, threads):
 def test_oversubscribed_ctas_are_clamped():
     """The persistent kernel needs every CTA resident: asking for more CTAs/SM than fit is clamped."""
     g = I.erdos_renyi_c1b()
-    r = gpu(g, ctas_per_sm=16, threads_per_cta=256)
+    r = gpu(g, ctas_per_sm=64, threads_per_cta=128)
     assert same(r, oracle.mbea(g))
 
 
