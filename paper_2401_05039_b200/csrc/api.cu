@@ -719,8 +719,9 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       for (int b = 0; b < 64; ++b)
         if (hg.busy_hist[b] || hg.exit_hist[b]) std::fprintf(stderr, " [%d] %llu/%llu", 2 * b, hg.busy_hist[b], hg.exit_hist[b]);
       std::fprintf(stderr, "\n");
-      for (int k = 0; k < 3; ++k) {
-        std::fprintf(stderr, "%s task warp-ms by completion time (2 ms buckets):", k == 0 ? "root" : (k == 1 ? "list" : "bitrow"));
+      for (int k = 0; k < 4; ++k) {
+        std::fprintf(stderr, "%s warp-ms by completion time (2 ms buckets):",
+                     k == 0 ? "root task" : (k == 1 ? "list task" : (k == 2 ? "bitrow task" : "failed steal")));
         for (int b = 0; b < 64; ++b)
           if (hg.tl_hist[k][b]) std::fprintf(stderr, " [%d] %.0f", 2 * b, hg.tl_hist[k][b] / 1.965e6);
         std::fprintf(stderr, "\n");

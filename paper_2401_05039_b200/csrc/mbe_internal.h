@@ -64,7 +64,7 @@ struct Globals {
   unsigned long long hist[2][32];    // MBE_STATS diagnostics: bit-row tasks by log2(|P|+|Q|) of their frame [0, 24) and by
                                      // log2(W) [24, 29): count, cycles
   unsigned long long exit_hist[64];  // MBE_STATS diagnostics: warps by exit time (2 ms buckets after launch)
-  unsigned long long tl_hist[3][64];  // MBE_STATS diagnostics: task cycles by completion time (2 ms buckets): root, list, bit-row
+  unsigned long long tl_hist[4][64];  // MBE_STATS diagnostics: cycles by completion time (2 ms buckets): root, list, bit-row tasks, steal+idle
   unsigned long long busy_hist[64];  // MBE_STATS diagnostics: warps registering idle for the first time, by time
 };
 

@@ -251,40 +251,19 @@ __device__ __forceinline__ bool row_any_and(const Row<W>& a, const Row<W>& b) {
 #ifndef MBE_AC_ROLL
 #define MBE_AC_ROLL 1
 #endif
-#ifndef MBE_SORT_ROLLED
-#define MBE_SORT_ROLLED 0
-#endif
+// n <= 32 pairs: rank sort (keys are unique), one rolled loop — a tiny instruction footprint
+// for the most frequent sort of the search (the P' candidates of a bit-row child).
 __device__ __noinline__ void sort_regs32(unsigned long long* key, uint32_t* val, uint32_t n, int lane) {
-  unsigned long long k = lane < (int)n ? key[lane] : ~0ull;
-  uint32_t v = lane < (int)n ? val[lane] : 0u;
-#if MBE_SORT_ROLLED
-  // rolled bitonic network over the next power of two >= n (instruction-cache footprint)
-  const int N = n <= 2 ? 2 : 1 << (32 - __clz((int)n - 1));
+  const bool mine = lane < (int)n;
+  const unsigned long long k = mine ? key[lane] : ~0ull;
+  const uint32_t v = mine ? val[lane] : 0u;
+  uint32_t rank = 0;
 #pragma unroll 1
-  for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll 1
-    for (int j = size >> 1; j > 0; j >>= 1) {
-#else
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int j = size >> 1; j > 0; j >>= 1) {
-#endif
-      unsigned long long ok = __shfl_xor_sync(FULLMASK, k, j);
-      uint32_t ov = __shfl_xor_sync(FULLMASK, v, j);
-      bool up = (lane & size) == 0;
-      bool lower = (lane & j) == 0;
-      bool take = lower ? (up ? ok < k : ok > k) : (up ? ok > k : ok < k);
-      if (take) {
-        k = ok;
-        v = ov;
-      }
-    }
-  }
+  for (uint32_t s = 0; s < n; ++s) rank += __shfl_sync(FULLMASK, k, s) < k ? 1u : 0u;
   __syncwarp();
-  if (lane < (int)n) {
-    key[lane] = k;
-    val[lane] = v;
+  if (mine) {
+    key[rank] = k;
+    val[rank] = v;
   }
   __syncwarp();
 }
@@ -2094,7 +2073,10 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         rot += 97;
       }
       if (!got) {
-        if (lane == 0 && MBE_STATS_ON) w.sm->ph[3] += clock64() - t0;
+        if (lane == 0 && MBE_STATS_ON) {
+          w.sm->ph[3] += clock64() - t0;
+          atomicAdd(&p.gl->tl_hist[3][min(63ull, (globaltimer_ns() - t_start) / 2000000ull)], clock64() - t0);
+        }
         unsigned long long t1 = stats_clock(p);
         __nanosleep(backoff);
         if (backoff < 2048) backoff <<= 1;
