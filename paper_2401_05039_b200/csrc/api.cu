@@ -704,10 +704,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       std::fprintf(stderr,
                    "longest list task: %.3f ms root=%llu x=%llu deg=%llu |L'|=%llu touched=%llu |P'|=%llu |Q'|=%llu "
                    "Wchild=%llu kept=%llu nP=%llu | isect %.3f scan %.3f classify %.3f sort %.3f child %.3f ms "
-                   "(dedup %.3f ms -> %llu rows, antichain %.3f ms)\n",
+                   "(before dedup %.3f ms, dedup %.3f ms -> %llu rows, antichain %.3f ms, prune %.3f ms = meta %.3f + eq %.3f + Q %.3f)\n",
                    L[0] / 1.965e6, L[1], L[2], L[3], L[4], L[5], L[6], L[7], L[8], L[14], L[15], L[9] / 1.965e6,
-                   L[10] / 1.965e6, L[11] / 1.965e6, L[12] / 1.965e6, L[13] / 1.965e6, L[16] / 1.965e6, L[18],
-                   L[17] / 1.965e6);
+                   L[10] / 1.965e6, L[11] / 1.965e6, L[12] / 1.965e6, L[13] / 1.965e6, L[20] / 1.965e6, L[16] / 1.965e6, L[18],
+                   L[17] / 1.965e6, L[19] / 1.965e6, L[21] / 1.965e6, L[22] / 1.965e6, L[23] / 1.965e6);
     }
     if (std::getenv("MBE_DEBUG_HIST") && (cfg.flags & MBE_STATS)) {
       for (int b = 0; b < 24; ++b)

@@ -60,7 +60,7 @@ struct Globals {
   unsigned long long max_task[4];  // MBE_STATS: longest single task (cycles): root, list, bit-row, -
   unsigned long long t_roots_out;  // MBE_STATS: ns after launch when the level-1 list ran out
   unsigned long long max_phase[16];  // MBE_STATS: longest single occurrence of each sub-phase (cycles)
-  unsigned long long longest[20];    // MBE_STATS diagnostics: the longest list-path task (see search.cu)
+  unsigned long long longest[24];    // MBE_STATS diagnostics: the longest list-path task (see search.cu)
   unsigned long long hist[2][32];    // MBE_STATS diagnostics: bit-row tasks by log2(|P|+|Q|) of their frame [0, 24) and by
                                      // log2(W) [24, 29): count, cycles
   unsigned long long exit_hist[64];  // MBE_STATS diagnostics: warps by exit time (2 ms buckets after launch)

@@ -578,6 +578,35 @@ __device__ __noinline__ uint32_t dedup_hash_rows(const uint32_t* src, uint32_t n
 
 // Same reduction for wide rows (8 or 16 words), word-sliced: rows are streamed from
 // memory (L1) instead of held in registers.
+#ifndef MBE_VEC_SUBSET
+#define MBE_VEC_SUBSET 0
+#endif
+#ifndef MBE_META54
+#define MBE_META54 1
+#endif
+#if MBE_VEC_SUBSET
+// Rows are 16-byte aligned and W is 8 or 16: all words are read with vector loads in flight at once.
+__device__ __forceinline__ bool wide_subset(const uint32_t* a, const uint32_t* b, uint32_t W) {  // a ⊆ b
+  uint32_t x = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < MBE_WMAX; q += 4)
+    if (q < W) {
+      const uint4 u = *reinterpret_cast<const uint4*>(a + q), v = *reinterpret_cast<const uint4*>(b + q);
+      x |= (u.x & ~v.x) | (u.y & ~v.y) | (u.z & ~v.z) | (u.w & ~v.w);
+    }
+  return x == 0u;
+}
+__device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, uint32_t W) {
+  uint32_t x = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < MBE_WMAX; q += 4)
+    if (q < W) {
+      const uint4 u = *reinterpret_cast<const uint4*>(a + q), v = *reinterpret_cast<const uint4*>(b + q);
+      x |= (u.x ^ v.x) | (u.y ^ v.y) | (u.z ^ v.z) | (u.w ^ v.w);
+    }
+  return x == 0u;
+}
+#else
 __device__ __forceinline__ bool wide_subset(const uint32_t* a, const uint32_t* b, uint32_t W) {  // a ⊆ b
   for (uint32_t q = 0; q < W; ++q)  // early exit: most non-subset pairs fail within a word or two
     if (a[q] & ~b[q]) return false;
@@ -588,10 +617,30 @@ __device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, ui
     if (a[q] != b[q]) return false;
   return true;
 }
+#endif
 
-// Wide-row antichain with cheap necessary-condition filters: a ⊆ b requires
-// popc(a) <= popc(b) and fold(a) ⊆ fold(b), fold = OR of the words.  Kept-row
-// (popc, fold) pairs live in shared memory (first 256 kept rows).
+// Necessary-condition filters for wide rows: a ⊆ b requires popc(a) <= popc(b) and
+// fold(a) ⊆ fold(b); a == b requires equal metadata.
+#if MBE_META54
+// fold = OR of the row's 64-bit halves (54 buckets kept); meta = (popc << 54) | fold
+#define MBE_META_SHIFT 54
+#define MBE_META_FOLD ((1ull << 54) - 1ull)
+__device__ __forceinline__ unsigned long long wide_meta(const uint32_t* r, uint32_t W) {
+  uint32_t pc = 0;
+  unsigned long long f = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < MBE_WMAX; q += 4)
+    if (q < W) {
+      const uint4 u = *reinterpret_cast<const uint4*>(r + q);
+      pc += __popc(u.x) + __popc(u.y) + __popc(u.z) + __popc(u.w);
+      f |= ((unsigned long long)u.y << 32 | u.x) | ((unsigned long long)u.w << 32 | u.z);
+    }
+  return ((unsigned long long)pc << 54) | (f & MBE_META_FOLD);
+}
+#else
+// fold = OR of the row's words; meta = (popc << 32) | fold
+#define MBE_META_SHIFT 32
+#define MBE_META_FOLD 0xffffffffull
 __device__ __forceinline__ unsigned long long wide_meta(const uint32_t* r, uint32_t W) {
   uint32_t pc = 0, f = 0;
   for (uint32_t q = 0; q < W; ++q) {
@@ -601,8 +650,9 @@ __device__ __forceinline__ unsigned long long wide_meta(const uint32_t* r, uint3
   }
   return ((unsigned long long)pc << 32) | f;
 }
+#endif
 __device__ __forceinline__ bool meta_may_subset(unsigned long long a, unsigned long long b) {
-  return (a >> 32) <= (b >> 32) && ((uint32_t)a & ~(uint32_t)b) == 0u;
+  return (a >> MBE_META_SHIFT) <= (b >> MBE_META_SHIFT) && (a & ~b & MBE_META_FOLD) == 0ull;
 }
 
 __device__ __noinline__ uint32_t antichain_wide(const uint32_t* src, uint32_t n, uint32_t* dst, uint32_t W, bool keep_all,
@@ -990,25 +1040,86 @@ __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t*
 // Wide rows (8/16 words): the same test word-sliced, rows read from memory (L1).  Every row's
 // (popcount, OR-fold) metadata is computed once into `meta` (global scratch, >= nP + nQ entries);
 // its necessary conditions for == and ⊆ filter the pairs, 8 Q rows in flight per step.
+#ifndef MBE_CMASK_MIN
+#define MBE_CMASK_MIN 0xffffffffu  // Q rows above which the wide check transposes Q into column masks (with >= 96 P rows)
+#endif
 __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t nP, const uint32_t* Qr, uint32_t nQ,
-                                                  uint32_t W, uint32_t* S, unsigned long long* meta, int lane) {
+                                                  uint32_t W, uint32_t* S, unsigned long long* meta,
+                                                  uint32_t* cmask_buf, int lane, unsigned long long* prof = nullptr) {
+  unsigned long long c0 = prof ? (unsigned long long)clock64() : 0ull, ca = 0, cb = 0;
   for (uint32_t t = lane; t < nP + nQ; t += 32)
     meta[t] = wide_meta(t < nP ? Pr + (size_t)t * W : Qr + (size_t)(t - nP) * W, W);
   __syncwarp();
+  if (prof) {
+    const unsigned long long c1 = (unsigned long long)clock64();
+    prof[0] = c1 - c0;
+    c0 = c1;
+  }
   const unsigned long long* mq = meta + nP;
+  // many Q rows: transpose them once into column masks, cmask[b * G + g] bit i = row 32g + i has
+  // column b (one ballot per column per 32 rows)
+  const uint32_t G = (nQ + 31) / 32;
+  uint32_t* cmask = (nQ > MBE_CMASK_MIN && nP >= 96) ? cmask_buf : nullptr;
+  if (cmask) {
+    for (uint32_t g = 0; g < G; ++g) {
+      const uint32_t i = 32u * g + lane;
+      for (uint32_t c = 0; c < W; ++c) {
+        const uint32_t wd = i < nQ ? Qr[(size_t)i * W + c] : 0u;
+        uint32_t mine = 0;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+          const uint32_t m = __ballot_sync(FULLMASK, (wd >> j) & 1u);
+          if (lane == j) mine = m;
+        }
+        cmask[(size_t)(32u * c + lane) * G + g] = mine;
+      }
+    }
+    __syncwarp();
+  }
   uint32_t nS = 0;
   for (uint32_t tb = 0; tb < nP; tb += 32) {
     const uint32_t t = tb + lane;
     bool alive = t < nP;
     const uint32_t* r = Pr + (size_t)(alive ? t : 0u) * W;
     const unsigned long long mr = alive ? meta[t] : 0ull;
-    const uint32_t key = (uint32_t)(mr >> 32);
+    const uint32_t key = (uint32_t)(mr >> MBE_META_SHIFT);
     for (int j = (int)t - 1; alive && j >= 0; --j) {
       const unsigned long long mj = meta[j];
-      if ((uint32_t)(mj >> 32) != key) break;
+      if ((uint32_t)(mj >> MBE_META_SHIFT) != key) break;
       if (mj == mr && wide_eq(r, Pr + (size_t)j * W, W)) alive = false;
     }
-    for (uint32_t qb = 0; qb < nQ; qb += 8) {
+    if (prof) {
+      __syncwarp();
+      const unsigned long long c1 = (unsigned long long)clock64();
+      ca += c1 - c0;
+      c0 = c1;
+    }
+    if (cmask) {
+      // (b) by column masks: the Q rows containing r_t are the AND over the set bits b of r_t of
+      // column b's row mask (one word per 32 Q rows, lanes over words)
+      uint32_t am = __ballot_sync(FULLMASK, alive);
+      while (am) {
+        const int sl = __ffs(am) - 1;
+        am &= am - 1;
+        const uint32_t* rs = Pr + (size_t)(tb + sl) * W;
+        bool hit = false;
+        for (uint32_t g0 = 0; g0 < G && !hit; g0 += 32) {
+          const uint32_t g = g0 + lane;
+          uint32_t acc = g < G ? 0xffffffffu : 0u;
+          for (uint32_t c = 0; c < W; ++c) {
+            uint32_t wd = rs[c];
+            while (wd) {
+              const uint32_t b = 32u * c + (uint32_t)(__ffs(wd) - 1);
+              wd &= wd - 1u;
+              if (g < G) acc &= cmask[(size_t)b * G + g];
+            }
+          }
+          hit = __any_sync(FULLMASK, acc != 0u);
+        }
+        if (hit && lane == sl) alive = false;
+      }
+    }
+    for (uint32_t qb = 0; !cmask && qb < nQ; qb += 8) {
       if (!__any_sync(FULLMASK, alive)) break;
       unsigned long long m8[8];
 #pragma unroll
@@ -1018,21 +1129,32 @@ __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t n
         if (alive && qb + u < nQ && meta_may_subset(mr, m8[u]) && wide_subset(r, Qr + (size_t)(qb + u) * W, W))
           alive = false;
     }
+    if (prof) {
+      __syncwarp();
+      const unsigned long long c1 = (unsigned long long)clock64();
+      cb += c1 - c0;
+      c0 = c1;
+    }
     const uint32_t b = __ballot_sync(FULLMASK, alive);
     if (alive) S[nS + __popc(b & lanemask_lt())] = t;
     nS += __popc(b);
   }
   __syncwarp();
+  if (prof) {
+    prof[1] = ca;
+    prof[2] = cb;
+  }
   return nS;
 }
 
 __device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr, uint32_t nP, const uint32_t* Qr,
-                                                  uint32_t nQ, uint32_t* S, unsigned long long* meta, int lane) {
+                                                  uint32_t nQ, uint32_t* S, unsigned long long* meta,
+                                                  uint32_t* cmask_buf, int lane, unsigned long long* prof = nullptr) {
   __syncwarp();
   if (W == 1) return prune_frame<1>(Pr, nullptr, nP, Qr, nQ, S, lane);
   if (W == 2) return prune_frame<2>(Pr, nullptr, nP, Qr, nQ, S, lane);
   if (W == 4) return prune_frame<4>(Pr, nullptr, nP, Qr, nQ, S, lane);
-  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, meta, lane);
+  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, meta, cmask_buf, lane, prof);
 }
 
 // Account the nP tasks of a child frame decided at build time (nS survive the check).
@@ -1088,7 +1210,8 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   unsigned long long tph = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
   const unsigned long long tstart = tph;
   unsigned long long tsub[5] = {0, 0, 0, 0, 0};
-  unsigned long long tdd[3] = {0, 0, 0};
+  unsigned long long tdd[5] = {0, 0, 0, 0, 0};
+  unsigned long long pprof[3] = {0, 0, 0};
   // Step 2: L' = L ∩ N(x)
   const uint32_t* Lp;
   uint32_t nLp;
@@ -1380,7 +1503,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       tdd[2] = qn;
     }
     uint32_t* S = CQ + (size_t)nQk * Wc;  // survivor list of the eager check
-    nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, lane);
+    const unsigned long long tp0 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
+    nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, w.pbuf, lane, MBE_STATS_ON ? pprof : nullptr);
+    if MBE_STATS_ON {
+      tdd[3] = (unsigned long long)clock64() - tp0;
+      tdd[4] = td0 - tph;
+    }
     account_children(w, p, nPc, nT, Wc, nQk);
     size = (uint64_t)(S + nT - C);
   } else {
@@ -1409,7 +1537,8 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       unsigned long long* L = p.gl->longest;
       L[1] = root ? 1ull : 0ull; L[2] = x; L[3] = dx; L[4] = nLp; L[5] = nt; L[6] = nPc; L[7] = nQc;
       L[8] = cbm ? Wc : 0ull; L[9] = tsub[0]; L[10] = tsub[1]; L[11] = tsub[2]; L[12] = tsub[3]; L[13] = tsub[4];
-      L[14] = nQk; L[15] = nP; L[16] = tdd[0]; L[17] = tdd[1]; L[18] = tdd[2];
+      L[14] = nQk; L[15] = nP; L[16] = tdd[0]; L[17] = tdd[1]; L[18] = tdd[2]; L[19] = tdd[3];
+      L[20] = tdd[4]; L[21] = pprof[0]; L[22] = pprof[1]; L[23] = pprof[2];
     }
   }
 }
@@ -1761,7 +1890,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   uint32_t* Stmp = w.touched;
   MBE_PHASE(14, tph);
   wide_sub(29);
-  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, lane);
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, w.pbuf, lane);
   MBE_PHASE(15, tph);
   wide_sub(30);
   account_children(w, p, nPc, nS, Wn, nQc);
