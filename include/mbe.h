@@ -63,7 +63,8 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t *row_ptr, const uint32
 #define MBE_STATS 0x2u        /* count algorithmic bytes / task kinds (small overhead) */
 #define MBE_NO_ANTICHAIN 0x4u /* keep every Q' row instead of the antichain (result-invariant, slower) */
 #define MBE_NO_TWIN 0x8u      /* disable root-level twin pre-pruning (result-invariant) */
-#define MBE_STEAL_ONE 0x10u   /* thieves take one task at a time instead of half a frame (result-invariant) */
+#define MBE_STEAL_ONE 0x10u   /* thieves take one task at a time (the default since round 1; kept for compatibility) */
+#define MBE_STEAL_HALF 0x20u  /* thieves take half of a frame's unclaimed tasks and copy the frame (result-invariant; slower on C2-C5) */
 
 typedef struct {
   uint32_t struct_size;      /* ABI versioning: sizeof(mbe_config) */
@@ -140,9 +141,12 @@ typedef struct {
 } mbe_graph_info;
 int mbe_get_info(const mbe_graph *g, mbe_graph_info *info);
 
-void mbe_free(mbe_graph *g);             /* NULL-safe; releases the graph's host and device memory */
+void mbe_free(mbe_graph *g);             /* NULL-safe; releases the graph's host memory and returns its device
+                                            block to a per-process cache reused by the next mbe_load_csr
+                                            (no cudaFree, which synchronises the device) */
 /* Search workspaces (per-warp scratch + frame arenas) are pooled per device and
- * reused across handles; this frees every pooled workspace not in use. */
+ * reused across handles; this frees every pooled workspace not in use and every
+ * cached graph block. */
 void mbe_release_workspaces(void);
 const char *mbe_strerror(int code);      /* static string */
 const char *mbe_last_error_detail(void); /* thread-local message of the last failing call */

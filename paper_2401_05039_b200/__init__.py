@@ -12,6 +12,7 @@ from ._lib import (  # noqa: F401
     MBE_NO_ANTICHAIN,
     MBE_NO_STEAL,
     MBE_NO_TWIN,
+    MBE_STEAL_HALF,
     MBE_STEAL_ONE,
     MBE_STATS,
     MBEError,

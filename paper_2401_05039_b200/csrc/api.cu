@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -51,6 +52,56 @@ struct DevBuf {
 
 thread_local uint64_t* g_upload_counter = nullptr;
 
+// Device blocks of freed graphs, kept for the next mbe_load_csr (a caching allocator: cudaFree
+// synchronises the device and was measured at 2-460 ms per mbe_free with the search workspaces
+// resident).  Returned to the driver by mbe_release_workspaces.
+struct CachedBlock {
+  int device;
+  void* p;
+  size_t bytes;
+};
+std::mutex g_graph_cache_mu;
+std::vector<CachedBlock> g_graph_cache;
+
+int graph_alloc(DevBuf& b, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_graph_cache_mu);
+    size_t best = SIZE_MAX;
+    for (size_t k = 0; k < g_graph_cache.size(); ++k) {
+      const CachedBlock& c = g_graph_cache[k];
+      if (c.device == dev && c.bytes >= bytes && c.bytes <= 2 * bytes + (1u << 20) &&
+          (best == SIZE_MAX || c.bytes < g_graph_cache[best].bytes))
+        best = k;
+    }
+    if (best != SIZE_MAX) {
+      b.p = g_graph_cache[best].p;
+      b.bytes = g_graph_cache[best].bytes;
+      g_graph_cache.erase(g_graph_cache.begin() + best);
+      return MBE_OK;
+    }
+  }
+  if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return fail(MBE_ENOMEM, "cudaMalloc graph");
+  }
+  b.bytes = bytes;
+  return MBE_OK;
+}
+
+void graph_release(DevBuf& b) {
+  if (b.p) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_graph_cache_mu);
+    g_graph_cache.push_back({dev, b.p, b.bytes});
+  }
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
 template <class T>
 int upload(DevBuf& b, const std::vector<T>& v) {
   size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
@@ -69,7 +120,7 @@ struct Side {
   DevBuf all;                   // one device allocation holding every array below
   DevBuf offU, adjU, offV, adjV, hvU, hvV, origUd, root_order, twin;  // views into `all` (not owned)
   void release() {
-    all.release();
+    graph_release(all);
     for (DevBuf* b : {&offU, &adjU, &offV, &adjV, &hvU, &hvV, &origUd, &root_order, &twin}) *b = DevBuf();
     built = false;
   }
@@ -85,11 +136,7 @@ struct Packer {
     total += (std::max<size_t>(bytes, 16) + 255) & ~size_t(255);
   }
   int commit(DevBuf& all, uint64_t* counter) {
-    if (cudaMalloc(&all.p, std::max<size_t>(total, 256)) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(MBE_ENOMEM, "cudaMalloc graph");
-    }
-    all.bytes = total;
+    if (int rc = graph_alloc(all, std::max<size_t>(total, 256))) return rc;
     std::vector<uint8_t> host(total);
     for (const Item& it : items) {
       if (it.src && it.bytes) std::memcpy(host.data() + it.off, it.src, it.bytes);
@@ -777,6 +824,17 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
 }
 
 void mbe_release_workspaces(void) {
+  {
+    std::lock_guard<std::mutex> lk(g_graph_cache_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (const CachedBlock& c : g_graph_cache) {
+      cudaSetDevice(c.device);
+      cudaFree(c.p);
+    }
+    g_graph_cache.clear();
+    cudaSetDevice(dev);
+  }
   std::lock_guard<std::mutex> lk(g_pool_mu);
   for (auto it = g_pool.begin(); it != g_pool.end();) {
     if (!(*it)->busy) {

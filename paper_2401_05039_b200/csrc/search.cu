@@ -53,6 +53,9 @@
 #ifndef MBE_SCAN_MLP
 #define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
 #endif
+#ifndef MBE_BACKOFF_MAX
+#define MBE_BACKOFF_MAX 32768  // ns: cap of an idle warp's exponential back-off between steal attempts
+#endif
 #ifndef MBE_CLS_MLP
 #define MBE_CLS_MLP 2   // touched-vertex slots in flight per lane during classification
 #endif
@@ -2198,7 +2201,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       bool got = false;
       if (steal) {
         // leaves the idle set only on a successful claim
-        got = try_steal(lane, gw, p, rot, !(p.flags & F_STEAL_ONE), &v, &vdep, &ti, &tend);
+        got = try_steal(lane, gw, p, rot, (p.flags & F_STEAL_HALF) && !(p.flags & F_STEAL_ONE), &v, &vdep, &ti, &tend);
         rot += 97;
       }
       if (!got) {
@@ -2208,7 +2211,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         }
         unsigned long long t1 = stats_clock(p);
         __nanosleep(backoff);
-        if (backoff < 2048) backoff <<= 1;
+        if (backoff < MBE_BACKOFF_MAX) backoff <<= 1;
         if (lane == 0 && MBE_STATS_ON) w.sm->ph[4] += clock64() - t1;
         continue;
       }

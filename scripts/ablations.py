@@ -1,0 +1,98 @@
+"""Ablations of the search kernel's design choices (the paper's E2/E3 analogues,
+P:655-731): every variant is result-invariant, so each run is also a parity check against the golden
+(count, hash, tasks) of tests/golden/configs.txt (oracle values).
+
+    python scripts/ablations.py C2 C5 [--reps 3] [--out profiles/ablations_r1.md]
+
+Variants: the default; bit-row threshold T = 256 / 128 / 32 (T = 32 leaves every frame with |L| > 32 on
+the reverse-scan list path, the closest to the paper's compact-array design); stealing off (paper: no
+WS); steal-half instead of single-task steals; antichain reduction of Q' off; root twin pruning off; the larger
+side as the candidate side (orientation, reading Z4); fewer resident warps (2 CTAs/SM).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2401_05039_b200 import (MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN,  # noqa: E402
+                                   MBE_STEAL_HALF, MBEGraph)
+from paper_2401_05039_b200 import inputs as I  # noqa: E402
+
+VARIANTS = [
+    ("default", {}),
+    ("T=256", dict(bitmap_threshold=256)),
+    ("T=128", dict(bitmap_threshold=128)),
+    ("T=32 (list path above one word)", dict(bitmap_threshold=32)),
+    ("no stealing", dict(flags=MBE_NO_STEAL)),
+    ("steal-half (copy the frame)", dict(flags=MBE_STEAL_HALF)),
+    ("no Q' antichain", dict(flags=MBE_NO_ANTICHAIN)),
+    ("no root twin pruning", dict(flags=MBE_NO_TWIN)),
+    ("larger side as candidates", dict(candidate_side=-1)),
+    ("2 CTAs/SM (8 warps/SM)", dict(ctas_per_sm=2)),
+]
+
+
+def golden():
+    out = {}
+    with open(os.path.join(ROOT, "tests", "golden", "configs.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            c, count, h, tasks = line.split()[:4]
+            out[c] = (int(count), int(h, 16), int(tasks))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="+")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    gold = golden()
+    rows = []
+    for c in a.configs:
+        g = I.config_graph(c)
+        smaller = 1 if g.n1 <= g.n2 else 2
+        with MBEGraph.from_graph(g) as G:
+            base = None
+            for name, kw in VARIANTS:
+                kw = dict(kw)
+                if kw.get("candidate_side") == -1:
+                    if max(g.n1, g.n2) > 200000:  # per-warp slot tables scale with the candidate side
+                        continue
+                    kw["candidate_side"] = 3 - smaller
+                G.enumerate(**kw)  # warm-up (and the other side's ingest, if any)
+                times, r = [], None
+                for _ in range(a.reps):
+                    r = G.enumerate(**kw)
+                    times.append(r.kernel_ms)
+                ms = min(times)
+                want = gold.get(c)
+                exact = want is None or (r.count, r.hash) == want[:2]
+                same_tree = want is None or r.tasks == want[2] or kw.get("candidate_side") or \
+                    (kw.get("flags", 0) & MBE_NO_TWIN)
+                if base is None:
+                    base = ms
+                row = dict(config=c, variant=name, kernel_ms=[round(t, 2) for t in times], best_ms=round(ms, 2),
+                           slowdown=round(ms / base, 3), count=r.count, hash=hex(r.hash), tasks=r.tasks,
+                           steals=r.steals, bit_exact=bool(exact), tree_as_oracle=bool(same_tree))
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                if not exact:
+                    raise SystemExit(f"{c} {name}: result differs from the oracle golden value")
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write("# Ablations (1 x B200, kernel ms = best of %d; every run bit-exact vs the oracle golden)\n\n" % a.reps)
+            f.write("Written by `scripts/ablations.py`. Slowdown is relative to the default of the same config.\n\n")
+            f.write("| config | variant | best ms | slowdown | tasks | steals |\n|---|---|---|---|---|---|\n")
+            for r in rows:
+                f.write(f"| {r['config']} | {r['variant']} | {r['best_ms']} | {r['slowdown']}x | {r['tasks']} | "
+                        f"{r['steals']} |\n")
+
+
+if __name__ == "__main__":
+    main()

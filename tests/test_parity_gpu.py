@@ -11,7 +11,8 @@ import pytest
 
 import oracle
 from oracle import reference as R
-from paper_2401_05039_b200 import MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN, MBE_STATS, MBE_STEAL_ONE, MBEGraph
+from paper_2401_05039_b200 import (MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN, MBE_STATS, MBE_STEAL_HALF, MBE_STEAL_ONE,
+                                   MBEGraph)
 from paper_2401_05039_b200 import inputs as I
 
 pytestmark = pytest.mark.gpu
@@ -98,7 +99,7 @@ def test_random_mid_graphs_both_sides(n, p):
 
 # ------------------------------------------------------------------ result invariance under every knob
 @pytest.mark.parametrize("T", [32, 64, 128, 256, 512])
-@pytest.mark.parametrize("flags", [0, MBE_NO_STEAL, MBE_STEAL_ONE, MBE_NO_ANTICHAIN | MBE_NO_TWIN, MBE_STATS])
+@pytest.mark.parametrize("flags", [0, MBE_NO_STEAL, MBE_STEAL_ONE, MBE_STEAL_HALF, MBE_NO_ANTICHAIN | MBE_NO_TWIN, MBE_STATS])
 def test_knobs_do_not_change_result_or_tree(T, flags):
     g = I.erdos_renyi_c1b()
     want = oracle.mbea(g)
@@ -120,7 +121,7 @@ def test_wide_bit_rows(g, T):
 def test_launch_shapes(ctas, threads):
     g = I.random_bipartite(200, 150, 0.06, 5)
     assert same(gpu(g, ctas_per_sm=ctas, threads_per_cta=threads), oracle.mbea(g))
-    assert same(gpu(g, ctas_per_sm=ctas, threads_per_cta=threads, flags=MBE_STEAL_ONE), oracle.mbea(g))
+    assert same(gpu(g, ctas_per_sm=ctas, threads_per_cta=threads, flags=MBE_STEAL_HALF), oracle.mbea(g))
 
 
 def test_oversubscribed_ctas_are_clamped():
