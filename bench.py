@@ -115,7 +115,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_ready(self, timeout: float = 3.0):
+        """nvidia-smi's start-up (NVML init) must not overlap the timed steps: wait for its first sample."""
+        t0 = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+
+    def window(self, t0: float, t1: float):
+        """Keep only the samples taken inside the timed region [t0, t1] (all of them if none fall inside)."""
+        self.t_window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -129,7 +139,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        lines = list(self.lines)
+        if getattr(self, "t_window", None):
+            inside = [x for x in lines if self.t_window[0] <= x[0] <= self.t_window[1]]
+            lines = inside or lines
+        for _, line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 6:
                 continue
@@ -276,12 +290,14 @@ def run_ours(args):
             c, h = r.count, r.hash
         return r, c, h
 
-    for _ in range(args.warmup):
-        flush.zero_()
-        step()
     times, kms, results = [], [], []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        clk.wait_ready()
+        for _ in range(args.warmup):
+            flush.zero_()
+            step()
+        t_timed = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()
             if world > 1:
@@ -295,6 +311,7 @@ def run_ours(args):
             times.append(max_over_ranks(ms, dev) if world > 1 else ms)
             kms.append(max_over_ranks(r.kernel_ms, dev) if world > 1 else r.kernel_ms)
             results.append((c, h))
+        clk.window(t_timed, time.perf_counter() + 0.15)
     assert all(x == results[0] for x in results), "result changed between steps"
     count, h = results[0]
     ms_per_step = float(np.mean(times))

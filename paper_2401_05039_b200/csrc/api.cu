@@ -19,6 +19,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/mbe.h"
@@ -51,6 +52,54 @@ struct DevBuf {
 };
 
 thread_local uint64_t* g_upload_counter = nullptr;
+
+// Host ingest threads: MBE_INGEST_THREADS, else min(hardware threads, 16); 1 for small graphs.
+unsigned ingest_threads(uint64_t work) {
+  if (const char* e = std::getenv("MBE_INGEST_THREADS")) return (unsigned)std::max(1, std::atoi(e));
+  if (work < (1u << 16)) return 1;
+  const unsigned h = std::thread::hardware_concurrency();
+  return std::min(16u, std::max(1u, h));
+}
+
+// fn(t, begin, end) over T contiguous ranges of [0, n); range t = [n t / T, n (t + 1) / T).
+template <class F>
+void parallel_ranges(uint64_t n, unsigned T, F&& fn) {
+  if (T <= 1 || n < T) {
+    fn(0u, (uint64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T - 1);
+  for (unsigned t = 1; t < T; ++t) th.emplace_back([&fn, n, T, t] { fn(t, n * t / T, n * (t + 1) / T); });
+  fn(0u, (uint64_t)0, n / T);
+  for (auto& x : th) x.join();
+}
+
+// fn(t, begin, end) over T vertex ranges of [0, n) holding about equal numbers of edges (off = CSR offsets,
+// n + 1 entries): power-law degrees put most edges on few vertices, so equal vertex counts load-imbalance.
+template <class Off, class F>
+void parallel_edges(const Off* off, uint64_t n, unsigned T, F&& fn) {
+  if (T <= 1 || n < T) {
+    fn(0u, (uint64_t)0, n);
+    return;
+  }
+  std::vector<uint64_t> cut(T + 1, n);
+  cut[0] = 0;
+  const uint64_t E = off[n] - off[0];
+  for (unsigned t = 1; t < T; ++t)
+    cut[t] = (uint64_t)(std::lower_bound(off, off + n + 1, (Off)(off[0] + E * t / T)) - off);
+  for (unsigned t = 1; t <= T; ++t) cut[t] = std::max(cut[t], cut[t - 1]);
+  std::vector<std::thread> th;
+  th.reserve(T - 1);
+  for (unsigned t = 1; t < T; ++t) th.emplace_back([&fn, &cut, t] { fn(t, cut[t], cut[t + 1]); });
+  fn(0u, cut[0], cut[1]);
+  for (auto& x : th) x.join();
+}
+
+// Pinned staging buffer for the one H2D copy of a side's packed arrays (kept across loads).
+std::mutex g_stage_mu;
+void* g_stage = nullptr;
+size_t g_stage_bytes = 0;
 
 // Device blocks of freed graphs, kept for the next mbe_load_csr (a caching allocator: cudaFree
 // synchronises the device and was measured at 2-460 ms per mbe_free with the search workspaces
@@ -137,14 +186,43 @@ struct Packer {
   }
   int commit(DevBuf& all, uint64_t* counter) {
     if (int rc = graph_alloc(all, std::max<size_t>(total, 256))) return rc;
-    std::vector<uint8_t> host(total);
     for (const Item& it : items) {
-      if (it.src && it.bytes) std::memcpy(host.data() + it.off, it.src, it.bytes);
       it.dst->p = static_cast<uint8_t*>(all.p) + it.off;
       it.dst->bytes = it.bytes;
       if (counter && it.src) *counter += it.bytes;
     }
-    CUDA_TRY(cudaMemcpy(all.p, host.data(), total, cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    if (g_stage_bytes < total) {
+      if (g_stage) cudaFreeHost(g_stage);
+      g_stage = nullptr;
+      g_stage_bytes = 0;
+      const size_t want = total + total / 4;
+      if (cudaHostAlloc(&g_stage, want, cudaHostAllocDefault) == cudaSuccess) {
+        g_stage_bytes = want;
+      } else {
+        cudaGetLastError();
+        g_stage = nullptr;
+      }
+    }
+    if (!g_stage) {  // no pinned memory: pageable copies straight from the arrays
+      for (const Item& it : items)
+        if (it.src && it.bytes) CUDA_TRY(cudaMemcpy(it.dst->p, it.src, it.bytes, cudaMemcpyHostToDevice));
+      return MBE_OK;
+    }
+    uint8_t* stage = static_cast<uint8_t*>(g_stage);
+    // parallel gather into the staging buffer: 1 MiB chunks of every item, dealt over the threads
+    std::vector<std::pair<size_t, size_t>> chunks;  // (item, byte offset in the item)
+    for (size_t k = 0; k < items.size(); ++k)
+      if (items[k].src)
+        for (size_t o = 0; o < items[k].bytes; o += (1u << 20)) chunks.push_back({k, o});
+    parallel_ranges(chunks.size(), ingest_threads(total / 4), [&](unsigned, uint64_t a, uint64_t b) {
+      for (uint64_t c = a; c < b; ++c) {
+        const Item& it = items[chunks[c].first];
+        const size_t o = chunks[c].second, n = std::min<size_t>(1u << 20, it.bytes - o);
+        std::memcpy(stage + it.off + o, static_cast<const uint8_t*>(it.src) + o, n);
+      }
+    });
+    CUDA_TRY(cudaMemcpy(all.p, stage, total, cudaMemcpyHostToDevice));
     return MBE_OK;
   }
 };
@@ -223,32 +301,46 @@ int build_side(mbe_graph* g, int s) {
   }
   S.maxdegU = maxdeg;
   lap("relabel");
-  // adjU[rank] = sorted V ids; adjV[v] = sorted ranks
-  std::vector<uint32_t> offU(nU + 1, 0), adjU(g->nE), offV(nV + 1, 0), adjV(g->nE);
+  // adjU[rank] = sorted V ids; adjV[v] = sorted ranks (the other direction's CSR mapped through
+  // rankU, each row re-sorted); all passes are parallel over vertex ranges
+  const unsigned nth = ingest_threads(g->nE);
+  if (dbg) std::fprintf(stderr, "    side ingest threads %u\n", nth);
+  const std::vector<uint32_t>& offO = s == 1 ? g->off2 : g->off1;  // other side's CSR (candidate ids)
+  const std::vector<uint32_t>& adjO = s == 1 ? g->adj2 : g->adj1;
+  std::vector<uint32_t> offU(nU + 1, 0), adjU(g->nE), offV(offO.begin(), offO.end()), adjV(g->nE);
   for (uint32_t r = 0; r < nU; ++r) {
-    uint32_t u = S.origU[r];
+    const uint32_t u = S.origU[r];
     offU[r + 1] = offU[r] + (offC[u + 1] - offC[u]);
-    std::copy(adjC.begin() + offC[u], adjC.begin() + offC[u + 1], adjU.begin() + offU[r]);
   }
-  for (uint64_t e = 0; e < g->nE; ++e) offV[adjU[e] + 1]++;
-  for (uint32_t v = 0; v < nV; ++v) offV[v + 1] += offV[v];
+  parallel_edges(offU.data(), nU, nth, [&](unsigned, uint64_t a, uint64_t b) {
+    for (uint64_t r = a; r < b; ++r) {
+      const uint32_t u = S.origU[r];
+      std::copy(adjC.begin() + offC[u], adjC.begin() + offC[u + 1], adjU.begin() + offU[r]);
+    }
+  });
+  lap("adjacency: offU + adjU");
+  parallel_edges(offV.data(), nV, nth, [&](unsigned, uint64_t a, uint64_t b) {
+    for (uint64_t v = a; v < b; ++v) {
+      for (uint32_t e = offV[v]; e < offV[v + 1]; ++e) adjV[e] = S.rankU[adjO[e]];
+      std::sort(adjV.begin() + offV[v], adjV.begin() + offV[v + 1]);
+    }
+  });
   // execution-order cost of each level-1 subtree (descending P-role 2-hop estimate):
-  //   cost(x) = Σ_{u ∈ N(x)} |{w ∈ N(u) : w > x}|
-  // filled in rank order, x lands at position k of adjV[u], so the term is deg(u) - k - 1 (O(E)).
+  //   cost(x) = Σ_{u ∈ N(x)} |{w ∈ N(u) : w > x}| = Σ_{u ∈ N(x)} deg(u) - k - 1, k = position of x in adjV[u]
+  lap("adjacency: adjV");
   std::vector<uint64_t> rcost(nU, 0);
-  {
-    std::vector<uint32_t> fill(offV.begin(), offV.end() - 1);
-    for (uint32_t r = 0; r < nU; ++r) {
+  parallel_edges(offU.data(), nU, nth, [&](unsigned, uint64_t a, uint64_t b) {
+    for (uint64_t r = a; r < b; ++r) {
       uint64_t c = 0;
       for (uint32_t e = offU[r]; e < offU[r + 1]; ++e) {
         const uint32_t u = adjU[e];
-        const uint32_t k = fill[u]++;
-        adjV[k] = r;
+        const uint32_t k = (uint32_t)(std::lower_bound(adjV.begin() + offV[u], adjV.begin() + offV[u + 1], (uint32_t)r) -
+                                      adjV.begin());
         c += offV[u + 1] - k - 1;
       }
       rcost[r] = c;
     }
-  }
+  });
   lap("adjacency");
   // hash terms: side bit 0 for side 1 (rows), 1 for side 2 (cols)
   std::vector<uint64_t> hvU(nU), hvV(nV);
@@ -264,7 +356,22 @@ int build_side(mbe_graph* g, int s) {
     const uint64_t c = std::min<uint64_t>(rcost[r], 0xffffffffull);
     key.push_back(((0xffffffffull - c) << 32) | r);
   }
-  std::sort(key.begin(), key.end());
+  {  // LSD radix sort, 16-bit digits (4 stable passes; std::sort took ~5 ms for 10^5 keys)
+    std::vector<uint64_t> tmp(key.size());
+    std::vector<uint32_t> cnt(1u << 16);
+    for (int sh = 0; sh < 64; sh += 16) {
+      std::fill(cnt.begin(), cnt.end(), 0u);
+      for (uint64_t k : key) cnt[(k >> sh) & 0xffffu]++;
+      uint32_t run = 0;
+      for (uint32_t& c : cnt) {
+        const uint32_t n = c;
+        c = run;
+        run += n;
+      }
+      for (uint64_t k : key) tmp[cnt[(k >> sh) & 0xffffu]++] = k;
+      key.swap(tmp);
+    }
+  }
   lap("root cost + sort");
   std::vector<uint32_t> order(key.size());
   for (size_t k = 0; k < key.size(); ++k) order[k] = (uint32_t)key[k];
@@ -457,27 +564,60 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
   g->device = device;
   g->n1 = n1;
   g->n2 = n2;
-  // row CSR, each row sorted + deduplicated (reading Z8)
+  // row CSR, each row sorted + deduplicated (reading Z8): every thread builds the rows of its range,
+  // then the ranges are concatenated at their prefix offsets
+  const unsigned nth = ingest_threads(nnz);
   g->off1.assign(n1 + 1, 0);
-  g->adj1.reserve(nnz);
-  for (uint32_t i = 0; i < n1; ++i) {
-    size_t b = g->adj1.size();
-    g->adj1.insert(g->adj1.end(), col_idx + row_ptr[i], col_idx + row_ptr[i + 1]);
-    if (!std::is_sorted(g->adj1.begin() + b, g->adj1.end())) std::sort(g->adj1.begin() + b, g->adj1.end());
-    g->adj1.erase(std::unique(g->adj1.begin() + b, g->adj1.end()), g->adj1.end());
-    g->off1[i + 1] = (uint32_t)g->adj1.size();
+  {
+    std::vector<std::vector<uint32_t>> loc(std::max(1u, nth));
+    std::vector<uint32_t> deg(n1);
+    std::vector<uint64_t> first(std::max(1u, nth) + 1, 0);  // first row of each thread's range
+    parallel_edges(row_ptr, n1, nth, [&](unsigned t, uint64_t a, uint64_t b) {
+      first[t] = a;
+      if (a >= b) return;
+      std::vector<uint32_t>& L = loc[t];
+      L.reserve(row_ptr[b] - row_ptr[a]);
+      for (uint64_t i = a; i < b; ++i) {
+        const size_t s0 = L.size();
+        L.insert(L.end(), col_idx + row_ptr[i], col_idx + row_ptr[i + 1]);
+        if (!std::is_sorted(L.begin() + s0, L.end())) std::sort(L.begin() + s0, L.end());
+        L.erase(std::unique(L.begin() + s0, L.end()), L.end());
+        deg[i] = (uint32_t)(L.size() - s0);
+      }
+    });
+    for (uint32_t i = 0; i < n1; ++i) g->off1[i + 1] = g->off1[i] + deg[i];
+    g->nE = g->off1[n1];
+    g->adj1.resize(g->nE);
+    parallel_ranges(std::max(1u, nth), std::max(1u, nth), [&](unsigned, uint64_t a, uint64_t b) {
+      for (uint64_t t = a; t < b; ++t) std::copy(loc[t].begin(), loc[t].end(), g->adj1.begin() + g->off1[first[t]]);
+    });
   }
-  g->nE = g->adj1.size();
   lap("row CSR sort+dedup");
-  // column CSR (counting sort; rows visited ascending -> sorted)
+  // column CSR: counting sort with per-thread column counts over row ranges (rows ascending within
+  // and across ranges -> every column's rows come out sorted)
   g->off2.assign(n2 + 1, 0);
   g->adj2.resize(g->nE);
-  for (uint32_t c : g->adj1) g->off2[c + 1]++;
-  for (uint32_t j = 0; j < n2; ++j) g->off2[j + 1] += g->off2[j];
   {
-    std::vector<uint32_t> fill(g->off2.begin(), g->off2.end() - 1);
-    for (uint32_t i = 0; i < n1; ++i)
-      for (uint32_t e = g->off1[i]; e < g->off1[i + 1]; ++e) g->adj2[fill[g->adj1[e]]++] = i;
+    const unsigned T = std::max(1u, std::min(nth, 8u));
+    std::vector<uint32_t> cnt((size_t)T * n2, 0);
+    parallel_edges(g->off1.data(), n1, T, [&](unsigned t, uint64_t a, uint64_t b) {
+      uint32_t* c = cnt.data() + (size_t)t * n2;
+      for (uint32_t e = g->off1[a]; e < g->off1[b]; ++e) c[g->adj1[e]]++;
+    });
+    for (uint32_t j = 0; j < n2; ++j) {
+      uint32_t run = g->off2[j];
+      for (unsigned t = 0; t < T; ++t) {
+        const uint32_t k = cnt[(size_t)t * n2 + j];
+        cnt[(size_t)t * n2 + j] = run;
+        run += k;
+      }
+      g->off2[j + 1] = run;
+    }
+    parallel_edges(g->off1.data(), n1, T, [&](unsigned t, uint64_t a, uint64_t b) {
+      uint32_t* c = cnt.data() + (size_t)t * n2;
+      for (uint64_t i = a; i < b; ++i)
+        for (uint32_t e = g->off1[i]; e < g->off1[i + 1]; ++e) g->adj2[c[g->adj1[e]]++] = (uint32_t)i;
+    });
   }
   lap("column CSR");
   if (cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
