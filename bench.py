@@ -261,6 +261,34 @@ def load_traffic(config):
     return None
 
 
+def load_ncu(config):
+    """Issue / SIMT / cache figures of the search kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p)).get(config)
+    if not d:
+        return None
+    m = d.get("metrics", {})
+
+    def num(k):
+        try:
+            return float(str(m[k]).split()[0])
+        except (KeyError, ValueError, IndexError):
+            return None
+
+    dur = d.get("duration_ms_under_ncu")
+    dram = d.get("dram_bytes_per_launch")
+    lane = num("smsp__thread_inst_executed_per_inst_executed.ratio")
+    return {"source": f"profiles/{d.get('name', config)}.md (one serialised launch under ncu)",
+            "dram_gbs": dram / dur / 1e6 if dram and dur else None,
+            "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "simt_lane_efficiency": lane / 32.0 if lane else None,
+            "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
+            "top_stalls_pct": dict(list(d.get("stall_pct", {}).items())[:3])}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -379,6 +407,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes, "kernel": "mbe_search_kernel"},
+            "ncu": load_ncu(args.config) if world == 1 else None,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "stats": {"tasks": st.tasks, "pruned": st.pruned, "list_tasks": st.list_tasks,

@@ -179,6 +179,30 @@ def test_metamorphic_transpose_isolated_duplicates():
     assert (gpu(gd).count, gpu(gd).hash) == (base.count, base.hash)
 
 
+@pytest.mark.parametrize("threads", ["1", "3", "16"])
+def test_parallel_ingest_unsorted_duplicate_rows(threads, monkeypatch):
+    """Host ingest split over threads (edge-balanced ranges; MBE_INGEST_THREADS forces the split on a
+    small graph): rows given unsorted with duplicates, empty rows and columns -> the oracle's result on
+    the deduplicated graph (reading Z8), for both candidate sides."""
+    monkeypatch.setenv("MBE_INGEST_THREADS", threads)
+    g = I.erdos_renyi_c1b(160, 120)
+    e = g.edges()
+    rng = np.random.default_rng(5)
+    rows = np.concatenate([e[:, 0], e[: len(e) // 3, 0]])
+    cols = np.concatenate([e[:, 1], e[: len(e) // 3, 1]])
+    n1, n2 = g.n1 + 7, g.n2 + 5  # isolated vertices on both sides
+    order = np.lexsort((rng.random(len(rows)), rows))  # grouped by row, shuffled inside each row
+    rows, cols = rows[order], cols[order]
+    row_ptr = np.zeros(n1 + 1, dtype=np.uint64)
+    row_ptr[1:] = np.cumsum(np.bincount(rows, minlength=n1)).astype(np.uint64)
+    want = oracle.mbea(I.from_edges(n1, n2, e[:, 0], e[:, 1]))
+    with MBEGraph(n1, n2, row_ptr, cols.astype(np.uint32)) as G:
+        assert G.info()["n_edges"] == len(e)
+        for side in (1, 2):
+            r = G.enumerate(candidate_side=side)
+            assert (r.count, r.hash) == (want.count, want.hash)
+
+
 # ------------------------------------------------------------------ per-root parity and multi-rank shares
 def test_per_root_sums_and_values_c1b():
     g = I.erdos_renyi_c1b()
