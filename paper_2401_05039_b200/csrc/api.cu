@@ -804,6 +804,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       p.ac_ratio = ar ? (uint32_t)std::strtoul(ar, nullptr, 10) : 0xffffffffu;
       const char* dm = std::getenv("MBE_DEDUP_MIN");
       p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 512u;
+      const char* df = std::getenv("MBE_DEFER_MIN");
+      p.defer_min = df ? (uint32_t)std::strtoul(df, nullptr, 10) : 65536u;
       const char* wa = std::getenv("MBE_WIDE_ACMAX");
       p.wide_acmax = wa ? (uint32_t)std::strtoul(wa, nullptr, 10) : 256u;
     }

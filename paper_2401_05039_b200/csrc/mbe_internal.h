@@ -77,6 +77,7 @@ struct SearchParams {
   uint32_t wide_qmax;
   uint32_t narrow_qmax, narrow_ratio;  // same guard for 1/2/4-word children (narrow_qmax 0 = always)
   uint32_t dedup_min;
+  uint32_t defer_min;   // wide list-path children with |P'| * |Q'| >= this defer Step 3 to each task (0 = never)
   uint32_t wide_acmax;  // wide (8/16-word) list-path children keep more distinct Q' rows than this unreduced
   uint32_t ac_min, ac_ratio;  // list-path children skip the antichain if |Q'| > ac_min and > ac_ratio*(|P'|+1)   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;

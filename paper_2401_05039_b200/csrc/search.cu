@@ -61,6 +61,7 @@
 #endif
 #define KIND_LIST 0u
 #define KIND_BITMAP 1u
+#define HDR_UNCHECKED (1u << 16)  // frame header flag: Step 3 not yet run for its tasks (each task runs it)
 #define TAG_R 0xffffffffu
 
 namespace {
@@ -1462,6 +1463,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   uint64_t size;
   uint32_t nQk = 0;
   uint32_t nT = nPc;  // tasks published (bit-row children: the survivors of the eager check)
+  bool deferred = false;  // bit-row child published unchecked (HDR_UNCHECKED)
   if (cbm) {
     uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
     for (uint32_t t = lane; t < nPc; t += 32) {
@@ -1507,12 +1509,21 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     }
     uint32_t* S = CQ + (size_t)nQk * Wc;  // survivor list of the eager check
     const unsigned long long tp0 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
-    nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, w.pbuf, lane, MBE_STATS_ON ? pprof : nullptr);
+    // A large wide child (a hub's level-1 frame) would make its eager check one warp's serial
+    // |P'| x |Q'| pass, the critical path of the whole launch on C2/C3: publish every task instead
+    // and let each task (spread over warps by stealing) run its own Step 3.
+    deferred = Wc >= 8 && p.defer_min && (uint64_t)nPc * nQk >= p.defer_min;
+    if (deferred) {
+      for (uint32_t t = lane; t < nPc; t += 32) S[t] = t;
+      nT = nPc;
+    } else {
+      nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, w.pbuf, lane, MBE_STATS_ON ? pprof : nullptr);
+      account_children(w, p, nPc, nT, Wc, nQk);
+    }
     if MBE_STATS_ON {
       tdd[3] = (unsigned long long)clock64() - tp0;
       tdd[4] = td0 - tph;
     }
-    account_children(w, p, nPc, nT, Wc, nQk);
     size = (uint64_t)(S + nT - C);
   } else {
     uint32_t* CK = CP + nPc;
@@ -1521,7 +1532,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   }
   if (nT > 0) {
     if (lane == 0) {
-      C[0] = (cbm ? KIND_BITMAP : KIND_LIST) | ((cbm ? Wc : 0u) << 8);
+      C[0] = (cbm ? KIND_BITMAP : KIND_LIST) | ((cbm ? Wc : 0u) << 8) | (deferred ? HDR_UNCHECKED : 0u);
       C[1] = nLp;
       C[2] = nPc;
       C[3] = nQk;
@@ -1784,7 +1795,28 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   __syncwarp();
   const uint32_t k = __reduce_add_sync(FULLMASK, lane < (int)W ? (uint32_t)__popc(lx[lane]) : 0u);
 
-  // Step 3 was decided when the frame was built (prune_frame_wide): this task is maximal.
+  if (F[0] & HDR_UNCHECKED) {
+    // Step 3 deferred to the task: x is not maximal iff a Q-role row (frame Q rows and
+    // the earlier siblings P[j < i]) contains row(x)
+    bool dom = false;
+    for (uint32_t tb = 0; tb < nQ + i && !dom; tb += 32) {
+      const uint32_t t = tb + lane;
+      bool sup = false;
+      if (t < nQ + i) {
+        const uint32_t* r = t < nQ ? Qrow + (size_t)t * W : Prow + (size_t)(t - nQ) * W;
+        sup = true;
+        for (uint32_t q = 0; q < W && sup; ++q) sup = (lx[q] & ~r[q]) == 0u;
+      }
+      dom = __any_sync(FULLMASK, sup);
+    }
+    account_task(w, p, dom);
+    if (lane == 0 && MBE_STATS_ON) {
+      w.bitmap_tasks++;
+      w.alg_bytes += 4ull * W * (1ull + nQ + i);
+    }
+    if (dom) return;
+  }
+  // Otherwise Step 3 was decided when the frame was built (prune_frame_wide): this task is maximal.
   MBE_PHASE(11, tph);
 
   // Step 4: expansion over P-role rows j > i (pbuf keeps the source row index of each P' candidate)

@@ -117,6 +117,19 @@ def test_wide_bit_rows(g, T):
     assert same(gpu(g, bitmap_threshold=T, flags=MBE_NO_ANTICHAIN), want)
 
 
+@pytest.mark.parametrize("g", [I.random_bipartite(12, 400, 0.7, 1), I.random_bipartite(40, 700, 0.3, 4),
+                               I.random_bipartite(30, 500, 0.5, 6)], ids=lambda g: g.name)
+@pytest.mark.parametrize("defer_min", ["1", "64"])
+def test_deferred_step3_on_wide_children(g, defer_min, monkeypatch):
+    """MBE_DEFER_MIN forces large wide list-path children to publish every task unchecked (each task
+    runs Step 3 itself): same tree (tasks, pruned) and result as the eager frame-build check."""
+    want = oracle.mbea(g)
+    monkeypatch.setenv("MBE_DEFER_MIN", defer_min)
+    assert same(gpu(g), want)
+    assert same(gpu(g, flags=MBE_STATS), want)
+    assert same(gpu(g, flags=MBE_STEAL_HALF), want)
+
+
 @pytest.mark.parametrize("ctas,threads", [(1, 32), (1, 128), (2, 128), (4, 64)])
 def test_launch_shapes(ctas, threads):
     g = I.random_bipartite(200, 150, 0.06, 5)
