@@ -48,7 +48,7 @@
 #define MBE_EXPORT(name) name
 #endif
 #ifndef MBE_NARROW_TEMPLATES
-#define MBE_NARROW_TEMPLATES 2  // bit mask: 2 / 4 = separate register-resident 2- / 4-word task bodies
+#define MBE_NARROW_TEMPLATES 0  // bit mask: 2 / 4 = separate register-resident 2- / 4-word task bodies (0: only 1-word; smaller code, C5 -2 %)
 #endif
 #ifndef MBE_SCAN_MLP
 #define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
