@@ -56,6 +56,9 @@
 #ifndef MBE_BACKOFF_MAX
 #define MBE_BACKOFF_MAX 32768  // ns: cap of an idle warp's exponential back-off between steal attempts
 #endif
+#ifndef MBE_COMPRESS_ROWS
+#define MBE_COMPRESS_ROWS 1  // wide column compression: rows per lane in flight (1 with a 2-way word unroll was best; 2 and 4 slower)
+#endif
 #ifndef MBE_CLS_MLP
 #define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification (2 -> 4: C5 80 -> 68 ms)
 #endif
@@ -935,36 +938,55 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
 __device__ __noinline__ void compress_rows_lanes(const uint32_t* F, const uint32_t* offs, uint32_t n, uint32_t W,
                                                  const uint32_t* lx, const uint32_t* cm, uint32_t Wn, uint32_t* dst,
                                                  int lane) {
-  for (uint32_t tb = 0; tb < n; tb += 32) {
-    const uint32_t t = tb + lane;
-    if (t < n) {
-      const uint32_t* src = F + offs[t];
-      uint32_t* out = dst + (size_t)t * Wn;
-      uint32_t acc = 0, accw = 0;
-#pragma unroll 4
-      for (uint32_t q = 0; q < W; ++q) {
-        const uint32_t m = lx[q];
-        uint32_t y = src[q] & m;
+  // MBE_COMPRESS_ROWS rows per lane at a time: their word loads are independent (latency overlap)
+  for (uint32_t tb = 0; tb < n; tb += 32 * MBE_COMPRESS_ROWS) {
+    const uint32_t* src[MBE_COMPRESS_ROWS];
+    uint32_t* out[MBE_COMPRESS_ROWS];
+    bool ok[MBE_COMPRESS_ROWS];
+    uint32_t acc[MBE_COMPRESS_ROWS], accw[MBE_COMPRESS_ROWS];
+#pragma unroll
+    for (int k = 0; k < MBE_COMPRESS_ROWS; ++k) {
+      const uint32_t t = tb + 32 * k + lane;
+      ok[k] = t < n;
+      src[k] = F + (ok[k] ? offs[t] : 0u);
+      out[k] = dst + (size_t)(ok[k] ? t : 0u) * Wn;
+      acc[k] = 0u;
+      accw[k] = 0u;
+    }
+#pragma unroll 2
+    for (uint32_t q = 0; q < W; ++q) {
+      const uint32_t m = lx[q];
+      uint32_t y[MBE_COMPRESS_ROWS];
+#pragma unroll
+      for (int k = 0; k < MBE_COMPRESS_ROWS; ++k) y[k] = ok[k] ? src[k][q] & m : 0u;
+      const uint32_t o = cm[80 + q], d = o >> 5, r = o & 31u;
+      const bool spill = r != 0u && r + __popc(m) > 32u;  // spills into the next output word
+#pragma unroll
+      for (int k = 0; k < MBE_COMPRESS_ROWS; ++k) {
 #pragma unroll
         for (int i = 0; i < 5; ++i) {
-          const uint32_t tt = y & cm[5 * q + i];
-          y = (y ^ tt) | (tt >> (1 << i));
+          const uint32_t tt = y[k] & cm[5 * q + i];
+          y[k] = (y[k] ^ tt) | (tt >> (1 << i));
         }
-        const uint32_t o = cm[80 + q], d = o >> 5, r = o & 31u;
-        if (d > accw) {  // the previous output word is complete
-          out[accw] = acc;
-          acc = 0;
-          accw = d;
+        if (d > accw[k]) {  // the previous output word is complete
+          if (ok[k]) out[k][accw[k]] = acc[k];
+          acc[k] = 0;
+          accw[k] = d;
         }
-        acc |= y << r;
-        if (r != 0u && r + __popc(m) > 32u) {  // spills into the next output word
-          out[accw] = acc;
-          acc = y >> (32u - r);
-          ++accw;
+        acc[k] |= y[k] << r;
+        if (spill) {
+          if (ok[k]) out[k][accw[k]] = acc[k];
+          acc[k] = y[k] >> (32u - r);
+          ++accw[k];
         }
       }
-      if (accw < Wn) out[accw++] = acc;
-      for (; accw < Wn; ++accw) out[accw] = 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < MBE_COMPRESS_ROWS; ++k) {
+      if (!ok[k]) continue;
+      uint32_t aw = accw[k];
+      if (aw < Wn) out[k][aw++] = acc[k];
+      for (; aw < Wn; ++aw) out[k][aw] = 0u;
     }
   }
   __syncwarp();
