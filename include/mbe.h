@@ -131,6 +131,20 @@ typedef struct {
  * subtrees; the shares of all ranks sum to the whole). */
 int mbe_enumerate(mbe_graph *g, const mbe_config *cfg, mbe_result *res, mbe_output *out);
 
+/* Canonical text of a bounded listing ("DESIGN DECISIONS":
+ * "one biclique per line, `L: id,id,... | R: id,id,...` with original input IDs, lines sorted
+ * lexicographically before writing").  Host-only post-processing, no device work.
+ *   out       : the mbe_output mbe_enumerate filled (caller-owned HOST buffers, read only).
+ *   n_records : records to format, normally res->records_written (<= out->cap_records).
+ *   buf, cap  : caller-owned HOST buffer of cap bytes; buf may be NULL when cap = 0 (size query).
+ *   *needed   : receives the exact text length in bytes (no NUL terminator is written).
+ * Each line is "L: " + the side-1 ids in decimal, comma-separated, in the record's order (ascending)
+ * + " | R: " + the side-2 ids likewise + "\n"; the lines are sorted by byte order (strcmp), so the
+ * text is identical for every config that enumerates the same set (records arrive unordered).
+ * Returns MBE_OK; MBE_EINVAL (NULL pointers, n_records > cap_records, a record outside ids[cap_ids]);
+ * MBE_EOVERFLOW if cap < *needed (buf untouched, *needed set); MBE_ENOMEM. */
+int mbe_format_listing(const mbe_output *out, uint64_t n_records, char *buf, uint64_t cap, uint64_t *needed);
+
 /* Static description of a loaded graph. */
 typedef struct {
   uint32_t n1, n2;

@@ -11,6 +11,9 @@
   SURVEY §8(c)): Σ H(A,B) mod 2^64 with
   H(A,B) = mix64(sA ^ rotl64(sB,32) ^ (|A|<<32) ^ |B|),
   sA = Σ mix64(2a), sB = Σ mix64(2b+1), a/b original 0-based ids of side 1/2.
+* ``listing_text`` — the canonical listing text of SPEC.md S:544 ("DESIGN
+  DECISIONS": one biclique per line, ``L: id,id,... | R: id,id,...`` with
+  original ids, lines sorted lexicographically), ids ascending within a side.
 
 Graphs are the row-CSR ``inputs.Graph`` objects (n1, n2, row_ptr, col_idx);
 this module only reads those arrays.
@@ -40,6 +43,15 @@ def biclique_hash(A, B) -> int:
 
 def result_hash(bicliques) -> int:
     return sum(biclique_hash(A, B) for A, B in bicliques) & MASK64
+
+
+def listing_text(bicliques) -> bytes:
+    """SPEC S:544 text: one line per (A, B), ids ascending per side, lines sorted bytewise."""
+    lines = []
+    for A, B in bicliques:
+        lines.append(("L: " + ",".join(str(a) for a in sorted(A)) + " | R: "
+                      + ",".join(str(b) for b in sorted(B)) + "\n").encode("ascii"))
+    return b"".join(sorted(lines))
 
 
 def _masks(g):

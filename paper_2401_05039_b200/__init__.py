@@ -20,7 +20,9 @@ from ._lib import (  # noqa: F401
     Result,
     load_library,
     make_config,
+    make_output,
     mbe_enumerate,
+    mbe_format_listing,
     mbe_free,
     mbe_get_info,
     mbe_last_error_detail,

@@ -23,7 +23,7 @@ MBE_OK, MBE_EINVAL, MBE_ENOMEM, MBE_ECUDA, MBE_EOVERFLOW, MBE_ERANGE, MBE_EDIST,
 MBE_NO_STEAL, MBE_STATS, MBE_NO_ANTICHAIN, MBE_NO_TWIN, MBE_STEAL_ONE, MBE_STEAL_HALF = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 
 EXPORTED_SYMBOLS = ("mbe_load_csr", "mbe_enumerate", "mbe_get_info", "mbe_free", "mbe_release_workspaces",
-                    "mbe_strerror", "mbe_last_error_detail")
+                    "mbe_strerror", "mbe_last_error_detail", "mbe_format_listing")
 
 _u32, _i32, _u64, _dbl, _vp = ctypes.c_uint32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 _p64, _p32 = ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)
@@ -92,6 +92,9 @@ def load_library():
             lib.mbe_strerror.restype = ctypes.c_char_p
             lib.mbe_last_error_detail.argtypes = []
             lib.mbe_last_error_detail.restype = ctypes.c_char_p
+            lib.mbe_format_listing.argtypes = [ctypes.POINTER(mbe_output), _u64, ctypes.c_char_p, _u64,
+                                               ctypes.POINTER(ctypes.c_uint64)]
+            lib.mbe_format_listing.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -177,6 +180,33 @@ def mbe_enumerate(handle: int, config: Optional[mbe_config] = None, output: Opti
                   float(res.roots_out_ms), tuple(int(v) for v in res.max_phase_cycles))
 
 
+def mbe_format_listing(output: mbe_output, n_records: int) -> bytes:
+    """Canonical listing text (include/mbe.h mbe_format_listing): size query, then format."""
+    lib = load_library()
+    need = ctypes.c_uint64(0)
+    rc = lib.mbe_format_listing(ctypes.byref(output), n_records, None, 0, ctypes.byref(need))
+    if rc not in (MBE_OK, MBE_EOVERFLOW):
+        raise MBEError(rc, "mbe_format_listing")
+    buf = ctypes.create_string_buffer(max(need.value, 1))
+    rc = lib.mbe_format_listing(ctypes.byref(output), n_records, buf, need.value, ctypes.byref(need))
+    if rc != MBE_OK:
+        raise MBEError(rc, "mbe_format_listing")
+    return buf.raw[:need.value]
+
+
+def make_output(cap_records: int, cap_ids: int):
+    """(mbe_output, keep-alive arrays rec_off, rec_n1, rec_n2, ids) over numpy host buffers."""
+    rec_off = np.zeros(max(cap_records, 1), dtype=np.uint64)
+    n1 = np.zeros(max(cap_records, 1), dtype=np.uint32)
+    n2 = np.zeros(max(cap_records, 1), dtype=np.uint32)
+    ids = np.zeros(max(cap_ids, 1), dtype=np.uint32)
+    out = mbe_output()
+    out.cap_records, out.cap_ids = cap_records, cap_ids
+    out.rec_off, out.rec_n1, out.rec_n2 = rec_off.ctypes.data_as(_p64), n1.ctypes.data_as(_p32), n2.ctypes.data_as(_p32)
+    out.ids = ids.ctypes.data_as(_p32)
+    return out, (rec_off, n1, n2, ids)
+
+
 def mbe_get_info(handle: int) -> dict:
     info = mbe_graph_info()
     rc = load_library().mbe_get_info(ctypes.c_void_p(handle), ctypes.byref(info))
@@ -222,20 +252,21 @@ class MBEGraph:
     def enumerate_list(self, cap_records: int = 1 << 20, cap_ids: int = 1 << 24, **cfg
                        ) -> Tuple[Result, List[Tuple[tuple, tuple]]]:
         """Bounded listing: (result, [(A side-1 ids, B side-2 ids), ...])."""
-        rec_off = np.zeros(max(cap_records, 1), dtype=np.uint64)
-        n1 = np.zeros(max(cap_records, 1), dtype=np.uint32)
-        n2 = np.zeros(max(cap_records, 1), dtype=np.uint32)
-        ids = np.zeros(max(cap_ids, 1), dtype=np.uint32)
-        out = mbe_output()
-        out.cap_records, out.cap_ids = cap_records, cap_ids
-        out.rec_off, out.rec_n1, out.rec_n2 = rec_off.ctypes.data_as(_p64), n1.ctypes.data_as(_p32), n2.ctypes.data_as(_p32)
-        out.ids = ids.ctypes.data_as(_p32)
+        out, (rec_off, n1, n2, ids) = make_output(cap_records, cap_ids)
         r = mbe_enumerate(self.handle, make_config(**cfg), out)
         recs = []
         for k in range(r.records_written):
             o, a, b = int(rec_off[k]), int(n1[k]), int(n2[k])
             recs.append((tuple(int(v) for v in ids[o:o + a]), tuple(int(v) for v in ids[o + a:o + a + b])))
         return r, recs
+
+    def enumerate_text(self, cap_records: int = 1 << 20, cap_ids: int = 1 << 24, **cfg) -> Tuple[Result, bytes]:
+        """Bounded listing as canonical text (mbe_format_listing)."""
+        out, keep = make_output(cap_records, cap_ids)
+        r = mbe_enumerate(self.handle, make_config(**cfg), out)
+        text = mbe_format_listing(out, r.records_written)
+        del keep
+        return r, text
 
     def close(self):
         if self.handle:

@@ -993,4 +993,49 @@ void mbe_release_workspaces(void) {
   }
 }
 
+// Canonical listing text: host post-processing of the
+// records mbe_enumerate wrote, so that listings of different configurations diff byte-exactly.
+int mbe_format_listing(const mbe_output* out, uint64_t n_records, char* buf, uint64_t cap, uint64_t* needed) {
+  if (!out || !needed) return fail(MBE_EINVAL, "out or needed is NULL");
+  if (n_records > out->cap_records) return fail(MBE_EINVAL, "n_records > cap_records");
+  if (n_records && (!out->rec_off || !out->rec_n1 || !out->rec_n2 || !out->ids))
+    return fail(MBE_EINVAL, "mbe_output buffer is NULL");
+  if (cap && !buf) return fail(MBE_EINVAL, "buf is NULL with cap > 0");
+  std::vector<std::string> lines;
+  try {
+    lines.resize(n_records);
+    for (uint64_t r = 0; r < n_records; ++r) {
+      const uint64_t o = out->rec_off[r], a = out->rec_n1[r], b = out->rec_n2[r];
+      if (o > out->cap_ids || a + b > out->cap_ids - o)
+        return fail(MBE_EINVAL, "record " + std::to_string(r) + " lies outside ids[cap_ids]");
+      std::string& s = lines[r];
+      s.reserve(8 + 8 * (a + b));
+      s += "L: ";
+      for (uint64_t i = 0; i < a; ++i) {
+        if (i) s += ',';
+        s += std::to_string(out->ids[o + i]);
+      }
+      s += " | R: ";
+      for (uint64_t i = 0; i < b; ++i) {
+        if (i) s += ',';
+        s += std::to_string(out->ids[o + a + i]);
+      }
+      s += '\n';
+    }
+    std::sort(lines.begin(), lines.end());  // byte order (std::string compares as unsigned char)
+  } catch (const std::bad_alloc&) {
+    return fail(MBE_ENOMEM, "listing text");
+  }
+  uint64_t total = 0;
+  for (const auto& s : lines) total += s.size();
+  *needed = total;
+  if (cap < total) return fail(MBE_EOVERFLOW, "listing text needs " + std::to_string(total) + " bytes");
+  uint64_t pos = 0;
+  for (const auto& s : lines) {
+    std::memcpy(buf + pos, s.data(), s.size());
+    pos += s.size();
+  }
+  return MBE_OK;
+}
+
 }  // extern "C"

@@ -110,3 +110,38 @@ def test_product_package_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "mbea_oracle" not in txt, f
+
+
+def test_format_listing_host_only_matches_oracle_text(lib):
+    """mbe_format_listing is host post-processing (no device): canonical text of records given in a
+    scrambled order equals the oracle's SPEC S:544 text; size query / overflow / bad record errors."""
+    import ctypes
+
+    import oracle
+    from oracle import reference as R
+    from paper_2401_05039_b200 import MBEError, inputs as I, make_output, mbe_format_listing
+
+    g = I.random_bipartite(12, 9, 0.4, 77)
+    recs = list(oracle.mbea_list(g))
+    rng = np.random.default_rng(5)
+    rng.shuffle(recs)
+    n_ids = sum(len(a) + len(b) for a, b in recs)
+    out, (rec_off, n1, n2, ids) = make_output(len(recs) + 3, n_ids + 7)
+    o = 0
+    for k, (a, b) in enumerate(recs):
+        rec_off[k], n1[k], n2[k] = o, len(a), len(b)
+        ids[o:o + len(a) + len(b)] = list(a) + list(b)
+        o += len(a) + len(b)
+    text = mbe_format_listing(out, len(recs))
+    assert text == R.listing_text(recs) and text.count(b"\n") == len(recs)
+    assert mbe_format_listing(out, 0) == b""
+    need = ctypes.c_uint64(0)
+    small = ctypes.create_string_buffer(4)
+    assert lib.mbe_format_listing(ctypes.byref(out), len(recs), small, 4, ctypes.byref(need)) == -4
+    assert need.value == len(text)
+    rec_off[0] = n_ids + 5  # record past cap_ids
+    with pytest.raises(MBEError) as e:
+        mbe_format_listing(out, len(recs))
+    assert e.value.code == -1
+    with pytest.raises(MBEError):
+        mbe_format_listing(out, len(recs) + 4)  # n_records > cap_records

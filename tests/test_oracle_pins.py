@@ -222,3 +222,19 @@ def test_invalid_input_rejected():
     bad2 = I.Graph(2, 2, np.array([0, 2, 1], dtype=np.uint64), np.array([0, 1], dtype=np.uint32))
     with pytest.raises(ValueError):
         oracle.mbea(bad2)
+
+
+# ------------------------------------------------------------------ listing text
+def test_listing_text_worked_example():
+    """SPEC.md S:544 ("DESIGN DECISIONS"): `L: id,... | R: id,...`, original ids, lines sorted
+    lexicographically (bytewise: "L: 1 " < "L: 10" < "L: 2").  Bicliques worked out by hand:
+    rows 0:{0,1}, 1:{1,2}, 2:{10}, 10:{5} -> ({0},{0,1}), ({0,1},{1}), ({1},{1,2}), ({10},{5}), ({2},{10})."""
+    g = I.from_edges(11, 11, [0, 0, 1, 1, 2, 10], [0, 1, 1, 2, 10, 5])
+    want = (b"L: 0 | R: 0,1\n"
+            b"L: 0,1 | R: 1\n"
+            b"L: 1 | R: 1,2\n"
+            b"L: 10 | R: 5\n"
+            b"L: 2 | R: 10\n")
+    assert R.listing_text(oracle.mbea_list(g)) == want
+    assert R.listing_text(R.maximal_bicliques_closure(g)) == want
+    assert R.listing_text([]) == b""

@@ -177,6 +177,19 @@ def test_listing_truncates_but_counts_stay_exact():
     assert set(recs) <= fam
 
 
+def test_listing_text_byte_exact_across_configs():
+    """the canonical listing text of the GPU path is byte-identical to
+    the oracle's, for every candidate side / stealing / threshold config."""
+    for g in [I.erdos_renyi_c1b(120, 80), I.crown(8), I.random_bipartite(40, 33, 0.3, 9)]:
+        want = R.listing_text(oracle.mbea_list(g))
+        with MBEGraph.from_graph(g) as G:
+            for cfg in ({}, {"candidate_side": 1}, {"candidate_side": 2}, {"flags": MBE_NO_STEAL},
+                        {"bitmap_threshold": 32, "ctas_per_sm": 1}):
+                r, text = G.enumerate_text(**cfg)
+                assert not r.truncated and r.records_written == r.count
+                assert text == want, cfg
+
+
 # ------------------------------------------------------------------ metamorphic
 def test_metamorphic_transpose_isolated_duplicates():
     g = I.erdos_renyi_c1b(150, 90)
