@@ -186,7 +186,7 @@ def _weighted_sampler(weights: np.ndarray):
 
 def power_law(n1: int, n2: int, n_edges: int, seed: int, gamma1: float, gamma2: float,
               i0_1: float = 1.0, i0_2: float = 1.0, blocks: int = 0, block_a: int = 30,
-              block_b: int = 15, block_p: float = 0.7, name: str = "") -> Graph:
+              block_b: int = 15, block_p: float = 0.7, block_uniform: bool = False, name: str = "") -> Graph:
     """Bipartite Chung-Lu with min degree 1 on both sides (SURVEY §8(d) recipe).
 
     * side-s weight of rank i: (i + i0_s)^(-1/(gamma_s - 1)); ranks are mapped to
@@ -195,13 +195,14 @@ def power_law(n1: int, n2: int, n_edges: int, seed: int, gamma1: float, gamma2: 
       weight-drawn vertex of the other side, then every still-isolated vertex of
       the smaller side gets one edge to a weight-drawn vertex of the larger side;
     * optional planted communities: ``blocks`` overlapping a x b blocks whose
-      members are drawn by weight, each pair an edge with prob ``block_p``;
+      members are drawn by weight (or uniformly with ``block_uniform``), each
+      pair an edge with prob ``block_p``;
     * then Chung-Lu pairs (both endpoints weight-drawn) until exactly
       ``n_edges`` distinct edges (first occurrences in counter order).
     """
     params = dict(n1=n1, n2=n2, n_edges=n_edges, seed=seed, gamma1=gamma1, gamma2=gamma2,
                   i0_1=i0_1, i0_2=i0_2, blocks=blocks, block_a=block_a, block_b=block_b,
-                  block_p=block_p)
+                  block_p=block_p, block_uniform=block_uniform)
     # rank -> id permutations
     perm1 = np.argsort(_rng_u64(seed, 1, np.arange(n1)), kind="stable")
     perm2 = np.argsort(_rng_u64(seed, 2, np.arange(n2)), kind="stable")
@@ -235,8 +236,14 @@ def power_law(n1: int, n2: int, n_edges: int, seed: int, gamma1: float, gamma2: 
     # 2) planted communities
     for b in range(blocks):
         base = b * (block_a + block_b + block_a * block_b)
-        ra = draw1(_uniform(seed, 5, base + np.arange(block_a)))
-        cb = draw2(_uniform(seed, 5, base + block_a + np.arange(block_b)))
+        ua = _uniform(seed, 5, base + np.arange(block_a))
+        ub = _uniform(seed, 5, base + block_a + np.arange(block_b))
+        if block_uniform:
+            ra = np.minimum((ua * n1).astype(np.int64), n1 - 1)
+            cb = np.minimum((ub * n2).astype(np.int64), n2 - 1)
+        else:
+            ra = draw1(ua)
+            cb = draw2(ub)
         pu = _uniform(seed, 5, base + block_a + block_b + np.arange(block_a * block_b))
         ii, jj = np.meshgrid(ra, cb, indexing="ij")
         m = (pu < block_p).reshape(block_a, block_b)
@@ -279,6 +286,14 @@ CONFIGS = {
                gamma1=2.1, gamma2=2.5, i0_1=16.0, i0_2=1.0, name="C4-bookcrossing"),
     "C5": dict(n1=545195, n2=96678, n_edges=1301942, seed=0x2401050390000005,
                gamma1=2.5, gamma2=2.1, i0_1=1.0, i0_2=16.0, name="C5-stackoverflow"),
+    # C5 with planted communities (SURVEY §8(d) "optional planted communities", §8(e) second scaling
+    # point): the same vertex sets and generator, plus 3,000 overlapping 30 x 15 blocks at p = 0.7
+    # (members drawn uniformly: weight-drawn members put every hub in hundreds of blocks and the
+    # oracle did not finish a 0.5 % root sample in 40 min), which lifts nMB/|E| toward the paper's community-rich datasets
+    # (P:627-630).  The blocks force ~1.5 M edges, so |E| is raised to 2,000,000.
+    "C5p": dict(n1=545195, n2=96678, n_edges=2000000, seed=0x2401050390000015,
+                gamma1=2.5, gamma2=2.1, i0_1=1.0, i0_2=16.0, blocks=3000, block_a=30, block_b=15,
+                block_p=0.7, block_uniform=True, name="C5p-stackoverflow-planted"),
 }
 
 

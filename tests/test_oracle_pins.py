@@ -238,3 +238,114 @@ def test_listing_text_worked_example():
     assert R.listing_text(oracle.mbea_list(g)) == want
     assert R.listing_text(R.maximal_bicliques_closure(g)) == want
     assert R.listing_text([]) == b""
+
+
+# ------------------------------------------------------------------ search-tree counters (tasks / pruned)
+# A task is one popped candidate x with L' = L ∩ N(x) ≠ ∅ (Algorithm 1 Steps 1-2); it is
+# pruned when Step 3 finds a Q vertex v with |N(v) ∩ L'| = |L'|.  Every candidate is
+# retired into Q after its iteration, and P' is ordered by ascending (|N(v) ∩ L'|, r(v)),
+# r = rank in the root order by (degree, original id) (reading Z6).  The
+# values below are derived by hand from those rules alone, so a flipped sort, a tie-break on the
+# original id instead of r(v), or a missing retirement of x into Q fails one of them.
+
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 7), (3, 5), (6, 2), (9, 9)])
+def test_tree_complete(m, n):
+    # K_{m,n}: candidates U_c = the smaller side (side 1 on a tie), all with N = V_c.  Root task 1:
+    # L' = V_c, Q = ∅, every other candidate has c = |L'| -> R', so P' = ∅.  Every later root task
+    # has the earlier candidates in Q with c = |L'| -> pruned.  (tasks, pruned) = (|U_c|, |U_c| - 1).
+    k = min(m, n)
+    r = oracle.mbea(I.complete(m, n))
+    assert (r.count, r.tasks, r.pruned) == (1, k, k - 1)
+
+
+@pytest.mark.parametrize("n", [1, 5, 17])
+def test_tree_matching(n):
+    # perfect matching: each root x has L' = {x's partner}, no other vertex meets it: n tasks, 0 pruned
+    r = oracle.mbea(I.perfect_matching(n))
+    assert (r.count, r.tasks, r.pruned) == (n, n, 0)
+
+
+def test_tree_star():
+    # star(6): one row joined to 6 cols; the row side (1 vertex) is the candidate side: one task
+    r = oracle.mbea(I.star(6))
+    assert (r.count, r.tasks, r.pruned) == (1, 1, 0)
+
+
+def test_tree_crown3():
+    # S_3, rows are candidates (tie -> side 1), N(0)={1,2}, N(1)={0,2}, N(2)={0,1}; all degree 2, so
+    # the root order is 0,1,2.
+    #  x=0: L'={1,2}, Q=∅; c(1)=|{2}|=1, c(2)=|{1}|=1 -> P'=[1,2]                     task 1
+    #     x=1: L''={2}; c(2)=0                                                       task 2
+    #     x=2: L''={1}; Q=[1]: c=0                                                   task 3
+    #  x=1: L'={0,2}; Q=[0]: c=1 -> Q'; c(2)=1 -> P'=[2]                             task 4
+    #     x=2: L''={0}; Q=[0]: c=0                                                   task 5
+    #  x=2: L'={0,1}; Q=[0,1]: c=1, c=1 -> Q'; P=∅                                   task 6
+    # 6 tasks, none pruned, 6 = 2^3 - 2 bicliques.
+    r = oracle.mbea(I.crown(3))
+    assert (r.count, r.tasks, r.pruned) == (6, 6, 0)
+
+
+def nested_pair():
+    """rows 0:{0,1,2}, 1:{0} (rows = candidates): the root order is by ascending degree."""
+    return I.from_edges(2, 3, [0, 0, 0, 1], [0, 1, 2, 0], name="nested_pair")
+
+
+def test_tree_root_order_ascending():
+    # r(1) = 0 (degree 1), r(0) = 1 (degree 3): root order [1, 0].
+    #  x=1: L'={0}, Q=∅; c(0)=1=|L'| -> R'; P'=∅                                      task 1
+    #  x=0: L'={0,1,2}; Q=[1]: c=1 < 3 -> Q'; P=∅                                      task 2
+    # (2, 0).  A descending root order gives x=0 first (P'=[1], one child task) and then x=1 pruned
+    # by Q=[0]: (3, 1).
+    r = oracle.mbea(nested_pair())
+    assert (r.count, r.tasks, r.pruned) == (2, 2, 0)
+
+
+def deep_order_graph():
+    """rows 0:{1,2,4}, 1:{0,2,3}, 2:{2,3,4}; 5 cols; rows are candidates (3 < 5)."""
+    return I.from_edges(3, 5, [0, 0, 0, 1, 1, 1, 2, 2, 2], [1, 2, 4, 0, 2, 3, 2, 3, 4], name="deep_order")
+
+
+def test_tree_deep_order_ascending():
+    # All degrees 3: root order 0,1,2 and r(v) = v.
+    #  x=0: L'={1,2,4}; c(1)=|{2}|=1, c(2)=|{2,4}|=2 -> P' ascending = [1, 2]         task 1
+    #     x=1: L''={2}; c(2)=1=|L''| -> R''                                           task 2
+    #     x=2: L''={2,4}; Q=[1]: c=1 < 2 -> Q'                                         task 3
+    #  x=1: L'={0,2,3}; Q=[0]: c=1 -> Q'; c(2)=|{2,3}|=2 -> P'=[2]                    task 4
+    #     x=2: L''={2,3}; Q=[0]: c=1 < 2                                               task 5
+    #  x=2: L'={2,3,4}; Q=[0,1]: c=2, c=2 < 3                                          task 6
+    # (6, 0).  A DESCENDING child order runs x=2 before x=1 under x=0: x=2 gets L''={2,4} and a
+    # child (x=1, L'''={2}), then x=1 (L''={2}) is pruned by Q=[2] (c=1=|L''|): (7, 1).
+    r = oracle.mbea(deep_order_graph())
+    assert (r.count, r.tasks, r.pruned) == (6, 6, 0)
+
+
+def tie_break_graph():
+    """rows 0:{0,1}, 1:{0,1,2}, 2:{0,1,3,4}, 3:{1,2,4}; 5 cols; rows are candidates (4 < 5)."""
+    return I.from_edges(4, 5, [0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3], [0, 1, 0, 1, 2, 0, 1, 3, 4, 1, 2, 4],
+                        name="tie_break")
+
+
+def test_tree_tie_break_by_rank():
+    # degrees 2,3,4,3 -> r(0)=0, r(1)=1, r(3)=2, r(2)=3; root order [0, 1, 3, 2].
+    #  x=0: L'={0,1}; c(1)=2, c(2)=2 -> R'; c(3)=|{1}|=1 -> P'=[3]                     task 1
+    #     x=3: L''={1}                                                                 task 2
+    #  x=1: L'={0,1,2}; Q=[0]: c=2 < 3 -> Q'; c(3)=|{1,2}|=2, c(2)=|{0,1}|=2 -> P'
+    #       keys tie at 2: r(3)=2 < r(2)=3 -> P'=[3, 2]                                 task 3
+    #     x=3: L''={1,2}; Q=[0]: c=1 -> Q'; c(2)=|{1}|=1 -> P'=[2]                      task 4
+    #        x=2: L'''={1}; Q=[0]: c=1=|L'''| -> pruned                                task 5 (pruned)
+    #     x=2: L''={0,1}; Q=[0,3]: c(0)=2=|L''| -> pruned                              task 6 (pruned)
+    #  x=3: L'={1,2,4}; Q=[0,1]: c=1, c=2 -> Q'; c(2)=|{1,4}|=2 -> P'=[2]              task 7
+    #     x=2: L''={1,4}; Q=[0,1]: c=1, c=1                                            task 8
+    #  x=2: L'={0,1,3,4}; Q=[0,1,3]: c=2,2,2 < 4                                       task 9
+    # (9, 2), 7 bicliques.  Breaking the tie by ORIGINAL id instead ([2, 3] under x=1) gives
+    # x=2 pruned at once (c(0)=2=|{0,1}|) and x=3 unpruned: (8, 1).
+    r = oracle.mbea(tie_break_graph())
+    assert (r.count, r.tasks, r.pruned) == (7, 9, 2)
+
+
+def test_tree_counters_literal_mbea_agrees_on_worked_graphs():
+    """The literal sequential MBEA(V, ∅, P, ∅) (no root shortcut) builds the same hand-derived trees."""
+    for g, want in [(nested_pair(), (2, 2, 0)), (deep_order_graph(), (6, 6, 0)), (tie_break_graph(), (7, 9, 2)),
+                    (I.crown(3), (6, 6, 0))]:
+        b = oracle.mbea_plain(g)
+        assert (b.count, b.tasks, b.pruned) == want, g.name

@@ -55,6 +55,17 @@ def test_closed_forms(g):
     assert same(gpu(g), oracle.mbea(g))
 
 
+def test_worked_tree_graphs():
+    """The hand-derived search trees of tests/test_oracle_pins.py (order-sensitive task counts)."""
+    from test_oracle_pins import deep_order_graph, nested_pair, tie_break_graph
+
+    for g, want in [(nested_pair(), (2, 2, 0)), (deep_order_graph(), (6, 6, 0)), (tie_break_graph(), (7, 9, 2)),
+                    (I.crown(3), (6, 6, 0))]:
+        r = gpu(g)
+        assert (r.count, r.tasks, r.pruned) == want, g.name
+        assert same(r, oracle.mbea(g)), g.name
+
+
 def test_empty_graphs():
     for n1, n2 in [(0, 0), (0, 5), (4, 0), (5, 7)]:
         r = gpu(I.from_edges(n1, n2, [], []))
