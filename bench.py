@@ -3,6 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one rank per GPU, NCCL)
 
+With --gpus N > 1 and no torchrun environment, bench.py starts the N ranks itself (127.0.0.1).
+Ranks claim level-1 subtrees dynamically from one counter in rank 0's device memory, shared by CUDA
+IPC (paper_2401_05039_b200/dist.py); ranks that share a GPU (fewer GPUs than ranks) reduce over gloo.
+
 A step = one full enumeration of the config's graph (every level-1 subtree,
 split over the ranks), with the graph resident in HBM.  Between timed steps a
 256 MiB buffer is written to flush L2 (the graph is L2-sized).  Times are CUDA
@@ -30,6 +34,7 @@ METRIC = "maximal bicliques/sec"
 UNIT = "bicliques/s"
 MASK64 = (1 << 64) - 1
 WORKLOADS = {
+    "C5p": "C5p synthetic power-law bipartite 545,195 x 96,678 with 3,000 planted 30x15 blocks (p=0.7), 2,000,000 edges",
     "C1": "C1a crown K12,12 minus a perfect matching (4094 bicliques)",
     "C1b": "C1b G(200,200,0.05), seed 0x2401050390000001",
     "C2": "C2 synthetic power-law bipartite 94,238 x 30,087, 293,360 edges (YouTube-membership-shaped)",
@@ -45,49 +50,9 @@ def graph_of(name):
     return I.crown(12) if name == "C1" else I.config_graph(name)
 
 
-# ------------------------------------------------------------------ distributed helpers (also unit-tested on gloo)
-def dist_env():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
-
-
-def limbs_of(count: int, h: int):
-    """(count, hash) -> 8 int64 limbs of 16 bits, so a sum over <= 2^47 ranks cannot overflow."""
-    out = []
-    for v in (count & MASK64, h & MASK64):
-        out += [(v >> (16 * k)) & 0xFFFF for k in range(4)]
-    return out
-
-
-def from_limbs(limbs):
-    vals = []
-    for j in range(2):
-        v = 0
-        for k in range(4):
-            v += int(limbs[4 * j + k]) << (16 * k)
-        vals.append(v & MASK64)
-    return vals[0], vals[1]
-
-
-def allreduce_result(count, h, device, group=None):
-    """Sum (count, hash mod 2^64) over ranks: the only data collective of the path (NCCL)."""
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor(limbs_of(count, h), dtype=torch.int64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return from_limbs(t.tolist())
-
-
-def max_over_ranks(x: float, device) -> float:
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor([x], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+# ------------------------------------------------------------------ distributed helpers (paper_2401_05039_b200/dist.py)
+from paper_2401_05039_b200.dist import (allreduce_result, dist_env, from_limbs, gather_floats, limbs_of,  # noqa: E402,F401
+                                        max_over_ranks, pick_backend, spawn_ranks)
 
 
 # ------------------------------------------------------------------ clocks
@@ -163,39 +128,42 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU oracle (cpu_baseline / reference arm)
 def oracle_rate(g, target_s: float, seed: int = 7, config: str = ""):
-    """Oracle bicliques/s on a bounded sample of level-1 subtrees.
+    """Oracle bicliques/s on a bounded, UNBIASED sample of the level-1 subtrees.
 
-    Per-root oracle cost is extremely heavy-tailed: on C2/C5 the heaviest 1% of roots (by 2-hop
-    size) hold ~90-95% of the oracle's work and single roots take minutes, so no small sample that
-    includes them has a bounded time.  The sample therefore EXCLUDES the heaviest 1% and takes every
-    k-th remaining root in cost order, as ONE oracle call (k calibrated by a pilot to ~target_s).
-    This flatters the CPU (several-fold); the recorded full-run oracle time is reported beside it.
+    The sample is a seeded uniform random 1/k of ALL level-1 subtrees (no exclusion): its expected
+    work and its expected count are both 1/k of the full run, so count/time estimates the full-run
+    rate.  Per-root oracle cost is extremely heavy-tailed (on C5 one subtree takes ~1 min on one
+    thread), so k is calibrated from the recorded full-run time when there is one (else by a pilot)
+    to make the expected wall time ~target_s on this host's cores; the sample's own time is reported.
     """
     import oracle
 
     side = 2 if g.n2 < g.n1 else 1
     n = g.n1 if side == 1 else g.n2
     threads = os.cpu_count() or 1
-    e = g.edges().astype(np.int64)
-    cand, other = (e[:, 0], e[:, 1]) if side == 1 else (e[:, 1], e[:, 0])
-    deg_other = np.bincount(other, minlength=g.n2 if side == 1 else g.n1)
-    proxy = np.bincount(cand, weights=deg_other[other], minlength=n)
-    order = np.argsort(proxy, kind="stable").astype(np.uint32)[: max(1, int(n * 0.99))]
+    deg = np.bincount(g.col_idx, minlength=g.n2) if side == 2 else np.diff(g.row_ptr.astype(np.int64))
+    roots = np.nonzero(deg > 0)[0].astype(np.uint32)
+    rng = np.random.default_rng(seed)
 
     def run(k):
-        roots = order[(seed % k)::k]
+        m = max(1, len(roots) // k)
+        pick = np.sort(rng.choice(len(roots), size=m, replace=False))
         t0 = time.perf_counter()
-        pr = oracle.mbea_roots(g, roots, candidate_side=side)
-        return int(pr[:, 0].sum()), time.perf_counter() - t0, len(roots)
+        pr = oracle.mbea_roots(g, roots[pick], candidate_side=side)
+        return int(pr[:, 0].sum()), time.perf_counter() - t0, m
 
-    k = max(1, len(order) // 400)
+    full = golden_full_run(config)
+    if full:
+        k = max(1, int(round(full["seconds"] * full["threads"] / threads / target_s)))
+    else:
+        k = max(1, len(roots) // 64)
+        _, dt, _ = run(k)
+        k = max(1, int(round(k * dt / target_s)))
     cnt, dt, m = run(k)
-    for _ in range(3):
-        if dt >= 0.5 * target_s or k == 1:
-            break
-        k = max(1, int(k * dt / target_s))
-        cnt, dt, m = run(k)
-    return cnt / dt, dict(count=cnt, seconds=dt, roots=m, frac=m / n, threads=threads, side=side, k=k)
+    sample = (f"seeded uniform random {m} of the {len(roots)} level-1 subtrees (1/{k}, no exclusion: unbiased for the "
+              f"full-run rate), {cnt} bicliques in {dt:.1f} s on {threads} threads")
+    return cnt / dt, dict(count=cnt, seconds=dt, roots=m, frac=m / max(1, len(roots)), threads=threads, side=side,
+                          k=k, sample=sample)
 
 
 def golden_full_run(config):
@@ -219,7 +187,7 @@ def run_reference(args):
 
     oracle.build_oracle()
     g = graph_of(args.config)
-    per_step_target = max(3.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    per_step_target = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     rates, infos = [], []
     for s in range(args.warmup + args.steps):
         r, info = oracle_rate(g, per_step_target, seed=7 + s, config=args.config)
@@ -228,21 +196,33 @@ def run_reference(args):
             infos.append(info)
     value = float(np.mean(rates))
     info = infos[-1]
-    sample = (f"{info['roots']} of the level-1 subtrees ({100 * info['frac']:.2f}%: every {info['k']}-th root in 2-hop-size "
-              f"order, heaviest 1% excluded), {info['count']} bicliques in {info['seconds']:.1f} s per step")
+    sample = info["sample"] + " per step"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([i["seconds"] for i in infos])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": WORKLOADS.get(args.config, args.config), "parallelism": "CPU threads over level-1 subtrees"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["threads"], "kind": "oracle", "sample": sample,
-                         "full_run": golden_full_run(args.config)},
+                         "cpu_model": cpu_model(), "full_run": golden_full_run(args.config)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
+D2H_BYTES = 112  # the hot prefix of the device Globals (count, hash, tasks, ...) copied back per call
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -293,34 +273,55 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2401_05039_b200 import MBE_STATS, MBEGraph, mbe_enumerate, mbe_free, mbe_get_info, mbe_load_csr
-    from paper_2401_05039_b200 import make_config
+    from paper_2401_05039_b200 import MBE_STATS, ClaimCounter, MBEGraph, mbe_enumerate, mbe_free, mbe_get_info
+    from paper_2401_05039_b200 import make_config, mbe_load_csr
+    from paper_2401_05039_b200.dist import RankLoop, share_counter
 
     world, rank, local = dist_env()
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback)")
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    backend = pick_backend(world, ndev) if world > 1 else None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    red_dev = dev if backend != "gloo" else "cpu"
     g = graph_of(args.config)
     stream = torch.cuda.current_stream(dev)
     knobs = dict(ctas_per_sm=args.ctas, threads_per_cta=args.threads, bitmap_threshold=args.T)
-    G = MBEGraph.from_graph(g, device=local)
+    G = MBEGraph.from_graph(g, device=dev_index)
+    # multi-rank: dynamic claiming through rank 0's counter (CUDA IPC); --static-deal: positions k = rank mod N
+    ctr = None
+    if world > 1 and not args.static_deal:
+        ctr = share_counter(dev_index, rank, lambda d: ClaimCounter(d), lambda d, h: ClaimCounter(d, handle=h))
+    loop = RankLoop(ctr, rank, world, red_dev) if ctr is not None else None
 
-    # one untimed stats pass: algorithmic bytes of this rank's share (deterministic search tree)
-    st = G.enumerate(flags=MBE_STATS, rank=rank, world=world, stream=stream.cuda_stream, **knobs)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    def enum(**extra):
+        kw = dict(rank=rank, world=world, stream=stream.cuda_stream, **knobs, **extra)
+        return G.enumerate(**kw)
 
     def step():
-        r = G.enumerate(rank=rank, world=world, stream=stream.cuda_stream, **knobs)
-        if world > 1:
-            c, h = allreduce_result(r.count, r.hash, dev)
-        else:
-            c, h = r.count, r.hash
-        return r, c, h
+        if loop is not None:
+            return loop.step(lambda cptr: enum(claim_counter=cptr))
+        r = enum()
+        c, h = allreduce_result(r.count, r.hash, red_dev) if world > 1 else (r.count, r.hash)
+        return c, h, r
 
-    times, kms, results = [], [], []
+    # one untimed stats pass (same claims protocol): algorithmic bytes of this rank's share
+    if loop is not None:
+        _, _, st = loop.step(lambda cptr: enum(claim_counter=cptr, flags=MBE_STATS))
+    else:
+        st = enum(flags=MBE_STATS)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    times, kms, results, per_rank = [], [], [], None
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         clk.wait_ready()
         for _ in range(args.warmup):
             flush.zero_()
@@ -328,53 +329,71 @@ def run_ours(args):
         t_timed = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()
+            if ctr is not None and rank == 0:
+                ctr.reset()
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize(dev)
             ev0.record(stream)
-            r, c, h = step()
+            if loop is not None:  # the counter was reset above, before the barrier
+                r = enum(claim_counter=ctr.ptr)
+                c, h = allreduce_result(r.count, r.hash, red_dev)
+            else:
+                c, h, r = step()
             ev1.record(stream)
             torch.cuda.synchronize(dev)
             ms = ev0.elapsed_time(ev1)
-            times.append(max_over_ranks(ms, dev) if world > 1 else ms)
-            kms.append(max_over_ranks(r.kernel_ms, dev) if world > 1 else r.kernel_ms)
+            times.append(max_over_ranks(ms, red_dev) if world > 1 else ms)
+            kms.append(max_over_ranks(r.kernel_ms, red_dev) if world > 1 else r.kernel_ms)
             results.append((c, h))
+            if world > 1:
+                per_rank = dict(kernel_ms=gather_floats(r.kernel_ms, red_dev, world),
+                                roots=[int(v) for v in gather_floats(float(r.roots_claimed), red_dev, world)],
+                                chunks=[int(v) for v in gather_floats(float(r.claim_chunks), red_dev, world)],
+                                count=[int(v) for v in gather_floats(float(r.count), red_dev, world)])
         clk.window(t_timed, time.perf_counter() + 0.15)
     assert all(x == results[0] for x in results), "result changed between steps"
     count, h = results[0]
-    ms_per_step = float(np.mean(times))
-    step_ms = [round(t, 3) for t in times]
-    value = count / (ms_per_step / 1e3)
+    ms_med = float(np.median(times))
+    value = count / (ms_med / 1e3)
 
-    # e2e through the public C ABI from host buffers: load (H2D) -> enumerate -> D2H result -> free
+    # e2e through the public C ABI from pinned host buffers: load (H2D) -> enumerate -> D2H result -> free
     rp = np.ascontiguousarray(g.row_ptr, dtype=np.uint64)
     ci = np.ascontiguousarray(g.col_idx, dtype=np.uint32)
     rp_pin = torch.from_numpy(rp).pin_memory().numpy()
     ci_pin = torch.from_numpy(ci).pin_memory().numpy()
     e2e_t, h2d = [], 0
     for k in range(args.warmup + args.steps):
+        if ctr is not None and rank == 0:
+            ctr.reset()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        hd = mbe_load_csr(g.n1, g.n2, rp_pin, ci_pin, device=local)
-        r = mbe_enumerate(hd, make_config(rank=rank, world=world, stream=stream.cuda_stream, **knobs))
+        hd = mbe_load_csr(g.n1, g.n2, rp_pin, ci_pin, device=dev_index)
+        cfg = make_config(rank=rank, world=world, stream=stream.cuda_stream,
+                          claim_counter=ctr.ptr if ctr is not None else 0, **knobs)
+        r = mbe_enumerate(hd, cfg)
         info = mbe_get_info(hd)
         mbe_free(hd)
         if world > 1:
-            allreduce_result(r.count, r.hash, dev)
+            ce, he = allreduce_result(r.count, r.hash, red_dev)
+        else:
+            ce, he = r.count, r.hash
+        assert (ce, he) == (count, h), "e2e result differs"
         dt = time.perf_counter() - t0
         if k >= args.warmup:
-            e2e_t.append(max_over_ranks(dt, dev) if world > 1 else dt)
+            e2e_t.append(max_over_ranks(dt, red_dev) if world > 1 else dt)
             h2d = int(info["h2d_bytes"])
-    e2e_value = count / float(np.mean(e2e_t))
+    e2e_value = count / float(np.median(e2e_t))
 
-    # roofline of the dominant kernel (the persistent search kernel)
-    alg_bytes = st.alg_bytes
-    kernel_ms = float(np.mean(kms))
+    # roofline of the dominant kernel (the persistent search kernel): SURVEY §8(d) algorithmic bytes of
+    # one launch (summed over ranks) / its CUDA-event time (max over ranks)
+    alg_bytes = float(st.alg_bytes)
+    kernel_ms = float(np.median(kms))
     if world > 1:
-        t = torch.tensor([alg_bytes], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([alg_bytes], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
         alg_bytes = float(t.item())
     peak, peak_src = load_peaks()
     achieved = alg_bytes / (kernel_ms / 1e3) / 1e9
@@ -386,37 +405,53 @@ def run_ours(args):
 
         oracle.build_oracle()
         rate, info = oracle_rate(g, args.cpu_seconds, config=args.config)
-        full = golden_full_run(args.config)
-        cpu = {"value": rate, "unit": UNIT, "cores": info["threads"], "kind": "oracle", "full_run": full,
-               "sample": f"{info['roots']} level-1 subtrees ({100 * info['frac']:.2f}%: every {info['k']}-th root in "
-                         f"2-hop-size order, heaviest 1% excluded, one oracle call), {info['count']} bicliques in {info['seconds']:.1f} s"}
+        cpu = {"value": rate, "unit": UNIT, "cores": info["threads"], "kind": "oracle", "cpu_model": cpu_model(),
+               "full_run": golden_full_run(args.config), "sample": info["sample"]}
     if rank == 0:
-        total_warps = st.n_warps
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_med, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOADS.get(args.config, args.config), "count": count, "hash": f"{h:#018x}",
-                       "candidate_side": st.candidate_side, "warps_per_gpu": total_warps,
+                       "candidate_side": st.candidate_side, "warps_per_gpu": st.n_warps,
                        "l2": "256 MiB buffer written between timed steps (graph fits in L2)",
-                       "parallelism": f"level-1 subtrees dealt over {world} rank(s); intra-GPU warp work stealing",
-                       "kernel_ms": kernel_ms, "step_ms": step_ms},
+                       "parallelism": (f"{world} rank(s) on {min(world, ndev)} GPU(s); level-1 subtrees "
+                                       + ("claimed in guided-self-scheduling chunks from rank 0's IPC counter"
+                                          if ctr is not None else ("dealt statically (k = rank mod N)" if world > 1
+                                                                   else "claimed by atomics"))
+                                       + "; intra-GPU warp work stealing; final all-reduce over "
+                                       + (backend or "-")),
+                       "statistic": "median of the timed steps (mean and p90 in step_stats)",
+                       "kernel_ms": kernel_ms, "step_ms": [round(t, 3) for t in times],
+                       "step_stats": {"median": ms_med, "mean": float(np.mean(times)),
+                                      "p90": float(np.percentile(times, 90)), "max": float(np.max(times))},
+                       "per_rank": per_rank},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 184, "ms_per_step": 1e3 * float(np.mean(e2e_t))},
-            "gpu_launches": 2 * args.steps,
+                    "d2h_bytes_per_step": D2H_BYTES, "ms_per_step": 1e3 * float(np.median(e2e_t))},
+            "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg_bytes, "kernel": "mbe_search_kernel"},
+                         "alg_bytes_per_launch": alg_bytes, "kernel": "mbe_search_kernel",
+                         "alg_bytes_rule": "SURVEY §8(d) per task (DESIGN.md §7): list task 4 deg(x) + 4 sum(deg(u)+1) "
+                                           "over L' + 8 |touched|; bit-row task 4 W (1 + |P| + |Q|) of its frame's "
+                                           "stored rows + 4 |P| ids; + 4 x child frame words"},
             "ncu": load_ncu(args.config) if world == 1 else None,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "stats": {"tasks": st.tasks, "pruned": st.pruned, "list_tasks": st.list_tasks,
                       "bitmap_tasks": st.bitmap_tasks, "frames": st.frames, "max_depth": st.max_depth,
                       "phase_frac": [round(c / max(1, st.n_warps * st.kernel_ms * 1.965e6), 4)
-                                     for c in st.phase_cycles[:15]]},
+                                     for c in st.phase_cycles[:16]],
+                      "alg_bytes_list_bitrow_write": list(st.alg_parts),
+                      "warp_busy_hist_5pct": list(st.busy_hist),
+                      "warp_busy_ms_min_mean_max": [round(v, 3) for v in st.busy_ms]},
         }
         print(json.dumps(line), flush=True)
     G.close()
+    if ctr is not None:
+        if world > 1:
+            dist.barrier()
+        ctr.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -435,9 +470,16 @@ def main():
     ap.add_argument("--T", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--static-deal", action="store_true", help="multi-rank: deal level-1 subtrees k = rank mod N")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        # no launcher: start the N ranks here (one process per rank, rendezvous on 127.0.0.1)
+        sys.exit(spawn_ranks(args.gpus, [os.path.abspath(__file__)] + sys.argv[1:]))
+    if world and world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -51,7 +51,8 @@ typedef struct mbe_graph mbe_graph;
  * (reading Z8); isolated vertices contribute nothing; n1 = 0, n2 = 0 or no
  * edges is a valid empty graph (count 0, hash 0).
  * The caller keeps ownership of both arrays (they are copied before return).
- * device: CUDA ordinal.  flags: reserved, pass 0.
+ * device: CUDA ordinal.  flags: bits 0-7 = host ingest threads (0 = auto: min(hardware threads, 16),
+ * 1 for small graphs); other bits reserved, pass 0.
  * Ingest builds both CSR directions (sorted, deduplicated),
  * relabels the candidate side by ascending (degree, original id) and uploads
  * everything to device memory owned by the handle. */
@@ -65,6 +66,8 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t *row_ptr, const uint32
 #define MBE_NO_TWIN 0x8u      /* disable root-level twin pre-pruning (result-invariant) */
 #define MBE_STEAL_ONE 0x10u   /* thieves take one task at a time (the default since round 1; kept for compatibility) */
 #define MBE_STEAL_HALF 0x20u  /* thieves take half of a frame's unclaimed tasks and copy the frame (result-invariant; slower on C2-C5) */
+#define MBE_ARENA_GROW 0x40u  /* arena_bytes is the INITIAL per-warp arena: grow it x4 and relaunch on overflow
+                                 (always the case when arena_bytes = 0) */
 
 typedef struct {
   uint32_t struct_size;      /* ABI versioning: sizeof(mbe_config) */
@@ -74,12 +77,25 @@ typedef struct {
   int32_t candidate_side;    /* 0 = auto (smaller side, ties: side 1), 1 = rows, 2 = cols; result-invariant */
   uint32_t flags;            /* MBE_* flags above */
   uint32_t rank, world;      /* this process' share of the level-1 subtrees (world >= 1) */
-  uint64_t *claim_counter;   /* device-visible u64 shared by all ranks (dynamic claiming; zero it before
-                                the first rank starts) or NULL (static deal: positions k = rank mod world) */
+  uint64_t *claim_counter;   /* shared root counter (dynamic claiming), or NULL (static deal:
+                                positions k = rank mod world).  Must be mapped on this device and be the
+                                same u64 for every rank: mbe_counter_ptr() of an mbe_counter created by one
+                                process and opened by the others (CUDA IPC; peer GPUs need P2P/NVLink).  It
+                                is advanced with system-scope atomics in chunks of
+                                ceil(remaining / (4 * world)) level-1 subtrees (guided self-scheduling); zero
+                                it (mbe_counter_reset) before the first rank of a run starts.  Every chunk a
+                                call claims is logged, so an arena-overflow relaunch replays exactly its own
+                                chunks: no subtree is lost or counted twice. */
   uint64_t arena_bytes;      /* per-warp frame arena; 0 = auto */
   void *stream;              /* cudaStream_t to run on; NULL = the legacy default stream */
   uint64_t *per_root;        /* optional HOST buffer [n_cand][4] = (count, hash, tasks, pruned) of each
                                 level-1 subtree, indexed by the candidate side's ORIGINAL id; or NULL */
+  uint32_t watchdog_ms;      /* no-progress watchdog: the call fails with MBE_EINTERNAL if no warp completes
+                                a task for this long (a hang is never silent).  0 = default (120000);
+                                0xffffffff = off.  It is not a limit on total run time. */
+  uint32_t defer_min;        /* wide (8/16-word) list-path children with |P'| * |Q'| >= defer_min publish every
+                                task with Step 3 deferred to the task (result-invariant); 0 = auto (65536),
+                                0xffffffff = never */
 } mbe_config;
 
 /* Optional bounded listing; caller-owned HOST buffers.  Record r occupies
@@ -104,7 +120,7 @@ typedef struct {
   int32_t candidate_side;   /* side actually used (1 or 2) */
   double kernel_ms;         /* device time of the search (CUDA events on the stream) */
   double wall_ms;           /* host time of the whole call */
-  uint64_t alg_bytes;       /* MBE_STATS: algorithmic bytes */
+  uint64_t alg_bytes;       /* MBE_STATS: algorithmic bytes (parts at the end of the struct) */
   uint64_t list_tasks;      /* MBE_STATS: tasks on the list (reverse-scan) path, incl. roots */
   uint64_t bitmap_tasks;    /* MBE_STATS: tasks on the bit-row path */
   uint64_t frames;          /* MBE_STATS: child frames pushed */
@@ -122,6 +138,18 @@ typedef struct {
   uint64_t max_task_cycles[3]; /* MBE_STATS: longest single task in cycles: [0] level-1, [1] list, [2] bit-row */
   double roots_out_ms;         /* MBE_STATS: time after launch when the level-1 subtree list ran out */
   uint64_t max_phase_cycles[16]; /* MBE_STATS: longest single occurrence of each phase_cycles sub-phase */
+  uint64_t roots_claimed;      /* level-1 subtrees this call ran (its share when ranks share a claim counter) */
+  uint32_t claim_chunks;       /* chunks it claimed from the shared counter (0 without one) */
+  uint32_t attempts;           /* kernel launches: 1 + arena-overflow relaunches */
+  /* MBE_STATS: per-warp workload distribution (the Fig. 5 analog): busy_hist[b] = warps whose
+   * busy share (cycles in tasks / cycles from launch to the warp's exit) lies in [b/20, (b+1)/20);
+   * busy_ms_min/max/mean = cycles in tasks per warp converted at the SM clock. */
+  uint32_t busy_hist[20];
+  double busy_ms_min, busy_ms_mean, busy_ms_max;
+  /* MBE_STATS: alg_bytes = alg_bytes_list + alg_bytes_bitrow + alg_bytes_write:
+   * list tasks 4 deg(x) + 4 Σ_{u∈L'}(deg(u)+1) + 8 |touched| + 4 (|L| + 2|P| + |R|); bit-row tasks
+   * 4 W (1 + |P| + |Q|) over their frame's stored rows (|Q| R1-reduced); child frames 4 x words written. */
+  uint64_t alg_bytes_list, alg_bytes_bitrow, alg_bytes_write;
 } mbe_result;
 
 /* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be
@@ -163,6 +191,22 @@ void mbe_free(mbe_graph *g);             /* NULL-safe; releases the graph's host
  * cached graph block. */
 void mbe_release_workspaces(void);
 const char *mbe_strerror(int code);      /* static string */
+
+/* Cross-process claim counter for dynamic claiming of level-1 subtrees over several ranks / GPUs
+ * (the paper's subtree fetch by atomics, lifted to one counter per box).
+ * One process creates it (device memory on its GPU, zeroed), exports the 64-byte CUDA IPC handle, and
+ * every other process opens that handle on its own device (a peer GPU needs P2P access, e.g. NVLink;
+ * another process on the same GPU also works).  mbe_counter_ptr() is what mbe_config.claim_counter takes.
+ * Errors: MBE_EINVAL (NULL arguments), MBE_ECUDA (allocation / IPC / peer mapping failed), MBE_EDIST
+ * (opening a handle in the process that created it). */
+typedef struct mbe_counter mbe_counter;
+int mbe_counter_create(int device, mbe_counter **out);
+int mbe_counter_ipc_handle(const mbe_counter *c, void *handle /* 64 bytes, caller-owned */);
+int mbe_counter_open(int device, const void *handle /* 64 bytes */, mbe_counter **out);
+uint64_t *mbe_counter_ptr(const mbe_counter *c); /* device-visible pointer, NULL if c is NULL */
+int mbe_counter_reset(mbe_counter *c, void *stream); /* zero it (stream-ordered; NULL = legacy stream), then sync */
+uint64_t mbe_counter_read(mbe_counter *c);          /* current value (synchronous), for diagnostics */
+void mbe_counter_close(mbe_counter *c);             /* NULL-safe; unmaps (opened) or frees (created) */
 const char *mbe_last_error_detail(void); /* thread-local message of the last failing call */
 
 #ifdef __cplusplus

@@ -9,6 +9,8 @@ missing (no CPU fallback).
 """
 from ._lib import (  # noqa: F401
     EXPORTED_SYMBOLS,
+    MBE_ARENA_GROW,
+    ClaimCounter,
     MBE_NO_ANTICHAIN,
     MBE_NO_STEAL,
     MBE_NO_TWIN,

@@ -21,9 +21,12 @@ LIB_PATH = os.environ.get("MBE_LIB_PATH") or os.path.join(_HERE, "libmbe.so")
 
 MBE_OK, MBE_EINVAL, MBE_ENOMEM, MBE_ECUDA, MBE_EOVERFLOW, MBE_ERANGE, MBE_EDIST, MBE_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7
 MBE_NO_STEAL, MBE_STATS, MBE_NO_ANTICHAIN, MBE_NO_TWIN, MBE_STEAL_ONE, MBE_STEAL_HALF = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+MBE_ARENA_GROW = 0x40
 
 EXPORTED_SYMBOLS = ("mbe_load_csr", "mbe_enumerate", "mbe_get_info", "mbe_free", "mbe_release_workspaces",
-                    "mbe_strerror", "mbe_last_error_detail", "mbe_format_listing")
+                    "mbe_strerror", "mbe_last_error_detail", "mbe_format_listing", "mbe_counter_create",
+                    "mbe_counter_ipc_handle", "mbe_counter_open", "mbe_counter_ptr", "mbe_counter_reset",
+                    "mbe_counter_read", "mbe_counter_close")
 
 _u32, _i32, _u64, _dbl, _vp = ctypes.c_uint32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p
 _p64, _p32 = ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)
@@ -33,7 +36,7 @@ class mbe_config(ctypes.Structure):
     _fields_ = [("struct_size", _u32), ("ctas_per_sm", _u32), ("threads_per_cta", _u32),
                 ("bitmap_threshold", _u32), ("candidate_side", _i32), ("flags", _u32), ("rank", _u32),
                 ("world", _u32), ("claim_counter", _vp), ("arena_bytes", _u64), ("stream", _vp),
-                ("per_root", _p64)]
+                ("per_root", _p64), ("watchdog_ms", _u32), ("defer_min", _u32)]
 
 
 class mbe_output(ctypes.Structure):
@@ -46,7 +49,10 @@ class mbe_result(ctypes.Structure):
                 ("records_written", _u64), ("truncated", _u32), ("candidate_side", _i32), ("kernel_ms", _dbl),
                 ("wall_ms", _dbl), ("alg_bytes", _u64), ("list_tasks", _u64), ("bitmap_tasks", _u64),
                 ("frames", _u64), ("n_warps", _u32), ("max_depth", _u32), ("phase_cycles", _u64 * 16),
-                ("max_task_cycles", _u64 * 3), ("roots_out_ms", _dbl), ("max_phase_cycles", _u64 * 16)]
+                ("max_task_cycles", _u64 * 3), ("roots_out_ms", _dbl), ("max_phase_cycles", _u64 * 16),
+                ("roots_claimed", _u64), ("claim_chunks", _u32), ("attempts", _u32), ("busy_hist", _u32 * 20),
+                ("busy_ms_min", _dbl), ("busy_ms_mean", _dbl), ("busy_ms_max", _dbl),
+                ("alg_bytes_list", _u64), ("alg_bytes_bitrow", _u64), ("alg_bytes_write", _u64)]
 
 
 class mbe_graph_info(ctypes.Structure):
@@ -95,6 +101,20 @@ def load_library():
             lib.mbe_format_listing.argtypes = [ctypes.POINTER(mbe_output), _u64, ctypes.c_char_p, _u64,
                                                ctypes.POINTER(ctypes.c_uint64)]
             lib.mbe_format_listing.restype = ctypes.c_int
+            lib.mbe_counter_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+            lib.mbe_counter_create.restype = ctypes.c_int
+            lib.mbe_counter_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
+            lib.mbe_counter_ipc_handle.restype = ctypes.c_int
+            lib.mbe_counter_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+            lib.mbe_counter_open.restype = ctypes.c_int
+            lib.mbe_counter_ptr.argtypes = [_vp]
+            lib.mbe_counter_ptr.restype = _vp
+            lib.mbe_counter_reset.argtypes = [_vp, _vp]
+            lib.mbe_counter_reset.restype = ctypes.c_int
+            lib.mbe_counter_read.argtypes = [_vp]
+            lib.mbe_counter_read.restype = _u64
+            lib.mbe_counter_close.argtypes = [_vp]
+            lib.mbe_counter_close.restype = None
             _lib = lib
     return _lib
 
@@ -121,6 +141,12 @@ class Result:
     max_task_cycles: tuple = ()
     roots_out_ms: float = -1.0
     max_phase_cycles: tuple = ()
+    roots_claimed: int = 0
+    claim_chunks: int = 0
+    attempts: int = 1
+    busy_hist: tuple = ()
+    busy_ms: tuple = ()  # (min, mean, max) task time per warp, MBE_STATS
+    alg_parts: tuple = ()  # (list, bit-row, frame writes) algorithmic bytes, MBE_STATS
 
 
 def mbe_strerror(code: int) -> str:
@@ -131,8 +157,10 @@ def mbe_last_error_detail() -> str:
     return load_library().mbe_last_error_detail().decode()
 
 
-def mbe_load_csr(n1: int, n2: int, row_ptr, col_idx, device: int = 0, flags: int = 0) -> int:
-    """Copy a HOST row-CSR (original ids) to the device; returns an opaque handle."""
+def mbe_load_csr(n1: int, n2: int, row_ptr, col_idx, device: int = 0, flags: int = 0, ingest_threads: int = 0) -> int:
+    """Copy a HOST row-CSR (original ids) to the device; returns an opaque handle.
+    ingest_threads: host threads of the ingest (flags bits 0-7; 0 = auto)."""
+    flags = (flags & ~0xFF) | (ingest_threads & 0xFF)
     lib = load_library()
     rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
     ci = np.ascontiguousarray(col_idx, dtype=np.uint32)
@@ -148,7 +176,7 @@ def mbe_load_csr(n1: int, n2: int, row_ptr, col_idx, device: int = 0, flags: int
 
 def make_config(ctas_per_sm: int = 0, threads_per_cta: int = 0, bitmap_threshold: int = 0, candidate_side: int = 0,
                 flags: int = 0, rank: int = 0, world: int = 1, claim_counter: int = 0, arena_bytes: int = 0,
-                stream: int = 0, per_root=None) -> mbe_config:
+                stream: int = 0, per_root=None, watchdog_ms: int = 0, defer_min: int = 0) -> mbe_config:
     c = mbe_config()
     c.struct_size = ctypes.sizeof(mbe_config)
     c.ctas_per_sm = ctas_per_sm
@@ -162,6 +190,8 @@ def make_config(ctas_per_sm: int = 0, threads_per_cta: int = 0, bitmap_threshold
     c.arena_bytes = arena_bytes
     c.stream = stream or None
     c.per_root = per_root.ctypes.data_as(_p64) if per_root is not None else None
+    c.watchdog_ms = watchdog_ms
+    c.defer_min = defer_min
     return c
 
 
@@ -177,7 +207,10 @@ def mbe_enumerate(handle: int, config: Optional[mbe_config] = None, output: Opti
                   int(res.list_tasks), int(res.bitmap_tasks), int(res.frames), int(res.n_warps),
                   int(res.max_depth), int(res.records_written), bool(res.truncated),
                   tuple(int(v) for v in res.phase_cycles), tuple(int(v) for v in res.max_task_cycles),
-                  float(res.roots_out_ms), tuple(int(v) for v in res.max_phase_cycles))
+                  float(res.roots_out_ms), tuple(int(v) for v in res.max_phase_cycles), int(res.roots_claimed),
+                  int(res.claim_chunks), int(res.attempts), tuple(int(v) for v in res.busy_hist),
+                  (float(res.busy_ms_min), float(res.busy_ms_mean), float(res.busy_ms_max)),
+                  (int(res.alg_bytes_list), int(res.alg_bytes_bitrow), int(res.alg_bytes_write)))
 
 
 def mbe_format_listing(output: mbe_output, n_records: int) -> bytes:
@@ -224,16 +257,67 @@ def mbe_release_workspaces() -> None:
     load_library().mbe_release_workspaces()
 
 
+class ClaimCounter:
+    """Cross-process claim counter (include/mbe.h mbe_counter_*): created by one rank, opened by the
+    others from its 64-byte CUDA IPC handle; ``ptr`` goes into mbe_config.claim_counter."""
+
+    def __init__(self, device: int = 0, handle: Optional[bytes] = None):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        if handle is None:
+            rc = lib.mbe_counter_create(int(device), ctypes.byref(h))
+            where = "mbe_counter_create"
+        else:
+            if len(handle) != 64:
+                raise ValueError("IPC handle must be 64 bytes")
+            rc = lib.mbe_counter_open(int(device), handle, ctypes.byref(h))
+            where = "mbe_counter_open"
+        if rc != MBE_OK:
+            raise MBEError(rc, where)
+        self.c = h.value
+        self.owner = handle is None
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        rc = load_library().mbe_counter_ipc_handle(ctypes.c_void_p(self.c), buf)
+        if rc != MBE_OK:
+            raise MBEError(rc, "mbe_counter_ipc_handle")
+        return buf.raw
+
+    @property
+    def ptr(self) -> int:
+        return load_library().mbe_counter_ptr(ctypes.c_void_p(self.c)) or 0
+
+    def reset(self, stream: int = 0) -> None:
+        rc = load_library().mbe_counter_reset(ctypes.c_void_p(self.c), ctypes.c_void_p(stream or None))
+        if rc != MBE_OK:
+            raise MBEError(rc, "mbe_counter_reset")
+
+    def read(self) -> int:
+        return int(load_library().mbe_counter_read(ctypes.c_void_p(self.c)))
+
+    def close(self) -> None:
+        if self.c:
+            load_library().mbe_counter_close(ctypes.c_void_p(self.c))
+            self.c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class MBEGraph:
     """RAII wrapper: a graph resident on one GPU."""
 
-    def __init__(self, n1: int, n2: int, row_ptr, col_idx, device: int = 0):
+    def __init__(self, n1: int, n2: int, row_ptr, col_idx, device: int = 0, ingest_threads: int = 0):
         self.n1, self.n2 = int(n1), int(n2)
-        self.handle = mbe_load_csr(n1, n2, row_ptr, col_idx, device)
+        self.handle = mbe_load_csr(n1, n2, row_ptr, col_idx, device, ingest_threads=ingest_threads)
 
     @classmethod
-    def from_graph(cls, g, device: int = 0) -> "MBEGraph":
-        return cls(g.n1, g.n2, g.row_ptr, g.col_idx, device)
+    def from_graph(cls, g, device: int = 0, ingest_threads: int = 0) -> "MBEGraph":
+        return cls(g.n1, g.n2, g.row_ptr, g.col_idx, device, ingest_threads)
 
     def info(self) -> dict:
         return mbe_get_info(self.handle)

@@ -52,10 +52,11 @@ struct DevBuf {
 };
 
 thread_local uint64_t* g_upload_counter = nullptr;
+thread_local unsigned g_ingest_threads = 0;  // mbe_load_csr flags bits 0-7 (0 = auto)
 
-// Host ingest threads: MBE_INGEST_THREADS, else min(hardware threads, 16); 1 for small graphs.
+// Host ingest threads: the mbe_load_csr flags request, else min(hardware threads, 16); 1 for small graphs.
 unsigned ingest_threads(uint64_t work) {
-  if (const char* e = std::getenv("MBE_INGEST_THREADS")) return (unsigned)std::max(1, std::atoi(e));
+  if (g_ingest_threads) return g_ingest_threads;
   if (work < (1u << 16)) return 1;
   const unsigned h = std::thread::hardware_concurrency();
   return std::min(16u, std::max(1u, h));
@@ -163,6 +164,8 @@ int upload(DevBuf& b, const std::vector<T>& v) {
 
 struct Side {
   bool built = false;
+  bool twin_ready = false;      // root twin flags computed (graph-only, once per side)
+  uint32_t auto_T = 0;          // cached auto bit-row threshold
   uint32_t nU = 0, nV = 0, n_roots = 0, maxdegU = 0;
   std::vector<uint32_t> origU;  // host copy: rank -> original id
   std::vector<uint32_t> rankU;  // host copy: original id -> rank
@@ -259,7 +262,10 @@ struct mbe_graph {
   SearchParams sp;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int sm_count = 0;
+  int occ[2][5] = {{0}};         // cached occupancy: [instr][threads/32 - 1] resident CTAs per SM
+  DevBuf claim_tab;             // shared-counter claim log of the current call ([n_roots + 1] u64)
   ~mbe_graph() {
+    claim_tab.release();
     for (auto& s : side) s.release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -535,7 +541,8 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
     std::fprintf(stderr, "  load %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(n - T).count());
     T = n;
   };
-  (void)flags;
+  if (flags & ~0xffu) return fail(MBE_EINVAL, "mbe_load_csr flags: only bits 0-7 (ingest threads) are defined");
+  g_ingest_threads = flags & 0xffu;
   if (!out) return fail(MBE_EINVAL, "out is NULL");
   *out = nullptr;
   if (!row_ptr && n1) return fail(MBE_EINVAL, "row_ptr is NULL");
@@ -693,22 +700,27 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     return MBE_OK;
   }
   const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : MBE_BLOCK;
-  // persistent kernel: every CTA must be co-resident, so clamp to the occupancy limit
+  // persistent kernel: every CTA must be co-resident, so clamp to the occupancy limit (cached per handle)
   // instrumented kernel instantiation only when stats / per-root counters / a listing are requested
   const bool instr = (cfg.flags & MBE_STATS) || cfg.per_root || (out && out->cap_records);
   const int smem_warp = instr ? mbe_search_smem_per_warp_instr() : mbe_search_smem_per_warp();
-  const int max_res = instr ? mbe_search_max_ctas_per_sm_instr((int)threads, smem_warp * (int)(threads / 32))
-                            : mbe_search_max_ctas_per_sm((int)threads, smem_warp * (int)(threads / 32));
-  if (max_res <= 0) return fail(MBE_ECUDA, "occupancy query failed for threads_per_cta=" + std::to_string(threads));
-  const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : (uint32_t)MBE_MINBLOCKS, (uint32_t)max_res);
+  int& occ = g->occ[instr ? 1 : 0][threads / 32 - 1];
+  if (occ <= 0)
+    occ = instr ? mbe_search_max_ctas_per_sm_instr((int)threads, smem_warp * (int)(threads / 32))
+                : mbe_search_max_ctas_per_sm((int)threads, smem_warp * (int)(threads / 32));
+  if (occ <= 0) return fail(MBE_ECUDA, "occupancy query failed for threads_per_cta=" + std::to_string(threads));
+  const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : (uint32_t)MBE_MINBLOCKS, (uint32_t)occ);
   const uint32_t grid = (uint32_t)g->sm_count * ctas_per_sm;
   const uint32_t n_warps = grid * (threads / 32);
-  // auto arena: proportional to the graph, 256 KiB .. 8 MiB per warp; grown x4 and retried on overflow
+  // auto arena: proportional to the graph, 256 KiB .. 8 MiB per warp; grown x4 and relaunched on overflow
+  const bool grow = cfg.arena_bytes == 0 || (cfg.flags & MBE_ARENA_GROW);
   uint64_t arena = cfg.arena_bytes ? cfg.arena_bytes
                                    : std::min<uint64_t>(8ull << 20, std::max<uint64_t>(256ull << 10, 16ull * (S.nU + S.nV + g->nE)));
   arena = (arena + 255) & ~255ull;
   // auto bit-row threshold: the widest rows (512 columns) whose workspace fits in 80% of free memory
+  // (decided once per loaded side; the free-memory query is not repeated on every call)
   uint32_t T = cfg.bitmap_threshold;
+  if (!T && S.auto_T) T = S.auto_T;
   if (!T) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
@@ -725,9 +737,33 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
         break;
       }
     }
+    S.auto_T = T;
   }
   const uint32_t wmax = mbe_words_for(T);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cfg.stream);
+  static const bool dbg_timing = std::getenv("MBE_DEBUG_TIMING") != nullptr;
+  static const bool dbg_longest = std::getenv("MBE_DEBUG_LONGEST") != nullptr;
+  static const bool dbg_hist = std::getenv("MBE_DEBUG_HIST") != nullptr;
+
+  // root twin flags: graph-only, computed once per loaded side (R2 at the root)
+  const DevGraph dg = {S.nU, S.nV, g->nE, (const uint32_t*)S.offU.p, (const uint32_t*)S.adjU.p,
+                       (const uint32_t*)S.offV.p, (const uint32_t*)S.adjV.p, (const uint64_t*)S.hvU.p,
+                       (const uint64_t*)S.hvV.p, (const uint32_t*)S.origUd.p, (const uint32_t*)S.root_order.p,
+                       (const uint8_t*)S.twin.p, S.n_roots, S.maxdegU};
+  if (!(cfg.flags & MBE_NO_TWIN) && !S.twin_ready) {
+    if (mbe_launch_twin(dg, g->sm_count, st) != 0)
+      return fail(MBE_ECUDA, std::string("twin kernel launch: ") + cudaGetErrorString(cudaGetLastError()));
+    S.twin_ready = true;
+  }
+  // claim log of a shared-counter call (one entry per claimed chunk, at most one per root)
+  if (cfg.claim_counter && g->claim_tab.bytes < 8ull * (S.n_roots + 1)) {
+    g->claim_tab.release();
+    if (cudaMalloc(&g->claim_tab.p, 8ull * (S.n_roots + 1)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MBE_ENOMEM, "claim log");
+    }
+    g->claim_tab.bytes = 8ull * (S.n_roots + 1);
+  }
 
   // listing buffers (device) for this call
   struct BufGuard {
@@ -752,7 +788,10 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     }
   } wg;
 
+  unsigned long long claim_state = 0;  // carried over to a relaunch: replays this call's claimed chunks
+  const bool want_stats = instr;
   for (int attempt = 0;; ++attempt) {
+    res->attempts = (uint32_t)attempt + 1;
     if (wg.w && wg.w->arena_bytes != arena) {
       checkin_workspace(wg.w);
       wg.w = nullptr;
@@ -763,61 +802,42 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
       if (rc) return rc;
     }
     Workspace* W = wg.w;
-    if (W->dirty && (rc = clear_tables(W, st))) return rc;
-    if (std::getenv("MBE_DEBUG_TIMING")) {
+    // a failed launch leaves slots, descriptors and stack tops dirty; a clean one leaves them zero
+    if (W->dirty) {
+      if ((rc = clear_tables(W, st))) return rc;
+      CUDA_TRY(cudaMemsetAsync(W->desc.p, 0, sizeof(Desc) * MBE_MAXDEPTH * n_warps, st));
+      CUDA_TRY(cudaMemsetAsync(W->tops.p, 0, 4ull * n_warps, st));
+    }
+    if (dbg_timing) {
       cudaStreamSynchronize(st);
       std::fprintf(stderr, "  enumerate: workspace checkout + clear %.2f ms (n_warps %u, T %u, arena %llu B, %.1f GB)\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count(), n_warps,
                    T, (unsigned long long)arena, W->ws.bytes / 1e9);
     }
     SearchParams& p = g->sp;
-    p.g.nU = S.nU;
-    p.g.nV = S.nV;
-    p.g.nE = g->nE;
-    p.g.offU = (const uint32_t*)S.offU.p;
-    p.g.adjU = (const uint32_t*)S.adjU.p;
-    p.g.offV = (const uint32_t*)S.offV.p;
-    p.g.adjV = (const uint32_t*)S.adjV.p;
-    p.g.hvU = (const uint64_t*)S.hvU.p;
-    p.g.hvV = (const uint64_t*)S.hvV.p;
-    p.g.origU = (const uint32_t*)S.origUd.p;
-    p.g.root_order = (const uint32_t*)S.root_order.p;
-    p.g.twin = (const uint8_t*)S.twin.p;
-    p.g.n_roots = S.n_roots;
-    p.g.maxdegU = S.maxdegU;
+    p.g = dg;
     p.cand_side = side;
     p.T = T;
-    {
-      const char* q = std::getenv("MBE_WIDE_QCAP");
-      p.wide_qcap = q ? (uint32_t)std::strtoul(q, nullptr, 10) : 256u;
-      const char* r = std::getenv("MBE_WIDE_RATIO");
-      p.wide_ratio = r ? (uint32_t)std::strtoul(r, nullptr, 10) : 64u;
-      const char* qm = std::getenv("MBE_WIDE_QMAX");
-      p.wide_qmax = qm ? (uint32_t)std::strtoul(qm, nullptr, 10) : 0xffffffffu;
-      const char* nq = std::getenv("MBE_NARROW_QMAX");
-      p.narrow_qmax = nq ? (uint32_t)std::strtoul(nq, nullptr, 10) : 0u;
-      const char* nr = std::getenv("MBE_NARROW_RATIO");
-      p.narrow_ratio = nr ? (uint32_t)std::strtoul(nr, nullptr, 10) : 256u;
-      const char* am = std::getenv("MBE_AC_MIN");
-      p.ac_min = am ? (uint32_t)std::strtoul(am, nullptr, 10) : 1024u;
-      const char* ar = std::getenv("MBE_AC_RATIO");
-      p.ac_ratio = ar ? (uint32_t)std::strtoul(ar, nullptr, 10) : 0xffffffffu;
-      const char* dm = std::getenv("MBE_DEDUP_MIN");
-      p.dedup_min = dm ? (uint32_t)std::strtoul(dm, nullptr, 10) : 512u;
-      const char* df = std::getenv("MBE_DEFER_MIN");
-      p.defer_min = df ? (uint32_t)std::strtoul(df, nullptr, 10) : 65536u;
-      const char* wa = std::getenv("MBE_WIDE_ACMAX");
-      p.wide_acmax = wa ? (uint32_t)std::strtoul(wa, nullptr, 10) : 256u;
-    }
+    p.wide_qcap = MBE_WIDE_QCAP;
+    p.wide_ratio = MBE_WIDE_RATIO;
+    p.wide_qmax = MBE_WIDE_QMAX;
+    p.narrow_qmax = MBE_NARROW_QMAX;
+    p.narrow_ratio = MBE_NARROW_RATIO;
+    p.ac_min = MBE_AC_MIN;
+    p.ac_ratio = MBE_AC_RATIO;
+    p.dedup_min = MBE_DEDUP_MIN;
+    p.defer_min = cfg.defer_min == 0 ? MBE_DEFER_MIN_DEFAULT : (cfg.defer_min == 0xffffffffu ? 0u : cfg.defer_min);
+    p.wide_acmax = MBE_WIDE_ACMAX;
     p.flags = cfg.flags;
     p.rank = cfg.rank;
     p.world = cfg.world;
     p.claim_counter = reinterpret_cast<unsigned long long*>(cfg.claim_counter);
+    p.claim_tab = static_cast<unsigned long long*>(g->claim_tab.p);
+    p.gss_div = 4u * cfg.world;
     p.n_warps = n_warps;
-    {
-      const char* wd = std::getenv("MBE_WATCHDOG_MS");
-      p.watchdog_ns = (wd ? std::strtoull(wd, nullptr, 10) : 120000ull) * 1000000ull;
-    }
+    p.watchdog_ns = cfg.watchdog_ms == 0xffffffffu
+                        ? 0ull
+                        : (unsigned long long)(cfg.watchdog_ms ? cfg.watchdog_ms : MBE_WATCHDOG_MS_DEFAULT) * 1000000ull;
     p.ws = static_cast<uint8_t*>(W->ws.p);
     p.ws_stride = W->stride;
     p.o_slot = W->o_slot;
@@ -845,10 +865,13 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.rec_n2 = (unsigned int*)lb.n2.p;
     p.out_ids = (unsigned int*)lb.ids.p;
 
-    CUDA_TRY(cudaMemsetAsync(W->gl.p, 0, sizeof(Globals), st));
-    CUDA_TRY(cudaMemsetAsync(&static_cast<Globals*>(W->gl.p)->t_roots_out, 0xff, 8, st));
-    CUDA_TRY(cudaMemsetAsync(W->desc.p, 0, sizeof(Desc) * MBE_MAXDEPTH * n_warps, st));
-    CUDA_TRY(cudaMemsetAsync(W->tops.p, 0, 4ull * n_warps, st));
+    Globals* dgl = static_cast<Globals*>(W->gl.p);
+    CUDA_TRY(cudaMemsetAsync(dgl, 0, want_stats ? sizeof(Globals) : MBE_GLOBALS_HOT_BYTES, st));
+    if (want_stats) {
+      CUDA_TRY(cudaMemsetAsync(&dgl->t_roots_out, 0xff, 8, st));
+      CUDA_TRY(cudaMemsetAsync(&dgl->warp_busy_min, 0xff, 8, st));
+    }
+    if (claim_state) CUDA_TRY(cudaMemcpyAsync(&dgl->claim_state, &claim_state, 8, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(W->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
     if (p.per_root) CUDA_TRY(cudaMemsetAsync(W->per_root.p, 0, 32ull * S.nU, st));
     const int smem = smem_warp * (int)(threads / 32);
@@ -857,17 +880,20 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     if (lrc != 0)
       return fail(MBE_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(cudaGetLastError()));
     Globals hg;
-    CUDA_TRY(cudaMemcpyAsync(&hg, W->gl.p, sizeof(Globals), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&hg, dgl, want_stats ? sizeof(Globals) : MBE_GLOBALS_HOT_BYTES, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    W->dirty = hg.error != 0;  // slots may hold partial counts, frames may be left on the stacks
     if (hg.error) {
-      W->dirty = true;  // slots may hold partial counts
-      if ((hg.error == 1u) && !cfg.arena_bytes && attempt < 6) {
-        arena *= 4;  // auto arena: grow and retry
+      if ((hg.error == 1u) && grow && attempt < 6) {
+        arena *= 4;  // grow and relaunch; a shared-counter call replays exactly the chunks it claimed
+        claim_state = hg.claim_state;
         continue;
       }
-      if (hg.error == 4u) return fail(MBE_EINTERNAL, "device watchdog expired (MBE_WATCHDOG_MS)");
+      if (hg.error == 4u)
+        return fail(MBE_EINTERNAL, "device watchdog: no task completed for " +
+                                       std::to_string(p.watchdog_ns / 1000000ull) + " ms (mbe_config.watchdog_ms)");
       if (hg.error == 3u)
         return fail(MBE_EINTERNAL, "device consistency check failed (info " + std::to_string(hg.err_info) + ")");
       return fail(MBE_EOVERFLOW, hg.error == 2u ? "stack depth > " + std::to_string(MBE_MAXDEPTH)
@@ -879,16 +905,33 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     res->pruned = hg.pruned;
     res->steals = hg.steals;
     res->kernel_ms = ms;
-    res->alg_bytes = hg.alg_bytes;
-    res->list_tasks = hg.list_tasks;
-    res->bitmap_tasks = hg.bitmap_tasks;
-    res->frames = hg.frames;
     res->n_warps = n_warps;
-    res->max_depth = hg.max_depth;
-    for (int k = 0; k < 16; ++k) res->phase_cycles[k] = hg.phase[k];
-    for (int k = 0; k < 3; ++k) res->max_task_cycles[k] = hg.max_task[k];
-    for (int k = 0; k < 16; ++k) res->max_phase_cycles[k] = hg.max_phase[k];
-    if (std::getenv("MBE_DEBUG_LONGEST") && (cfg.flags & MBE_STATS)) {
+    res->roots_claimed = hg.roots_run;
+    res->claim_chunks = cfg.claim_counter ? (uint32_t)(hg.claim_state >> 33) : 0u;
+    if (want_stats) {
+      res->alg_bytes = hg.alg_bytes;
+      res->alg_bytes_list = hg.alg_list;
+      res->alg_bytes_bitrow = hg.alg_bitrow;
+      res->alg_bytes_write = hg.alg_write;
+      res->list_tasks = hg.list_tasks;
+      res->bitmap_tasks = hg.bitmap_tasks;
+      res->frames = hg.frames;
+      res->max_depth = hg.max_depth;
+      for (int k = 0; k < 16; ++k) res->phase_cycles[k] = hg.phase[k];
+      for (int k = 0; k < 3; ++k) res->max_task_cycles[k] = hg.max_task[k];
+      for (int k = 0; k < 16; ++k) res->max_phase_cycles[k] = hg.max_phase[k];
+      res->roots_out_ms = hg.t_roots_out == ~0ull ? -1.0 : (double)hg.t_roots_out * 1e-6;
+      int clk_khz = 0;
+      cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, g->device);
+      const double cyc_per_ms = clk_khz > 0 ? (double)clk_khz : 1.965e6;
+      for (int b = 0; b < 20; ++b) res->busy_hist[b] = (uint32_t)hg.warp_busy_hist[b];
+      res->busy_ms_min = hg.warp_busy_min == ~0ull ? 0.0 : (double)hg.warp_busy_min / cyc_per_ms;
+      res->busy_ms_max = (double)hg.warp_busy_max / cyc_per_ms;
+      res->busy_ms_mean = (double)hg.warp_busy_sum / cyc_per_ms / (double)n_warps;
+    } else {
+      res->roots_out_ms = -1.0;
+    }
+    if (dbg_longest && (cfg.flags & MBE_STATS)) {
       const unsigned long long* L = hg.longest;
       std::fprintf(stderr,
                    "longest list task: %.3f ms root=%llu x=%llu deg=%llu |L'|=%llu touched=%llu |P'|=%llu |Q'|=%llu "
@@ -898,7 +941,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
                    L[10] / 1.965e6, L[11] / 1.965e6, L[12] / 1.965e6, L[13] / 1.965e6, L[20] / 1.965e6, L[16] / 1.965e6, L[18],
                    L[17] / 1.965e6, L[19] / 1.965e6, L[21] / 1.965e6, L[22] / 1.965e6, L[23] / 1.965e6);
     }
-    if (std::getenv("MBE_DEBUG_HIST") && (cfg.flags & MBE_STATS)) {
+    if (dbg_hist && (cfg.flags & MBE_STATS)) {
       for (int b = 0; b < 24; ++b)
         if (hg.hist[0][b])
           std::fprintf(stderr, "bit-row tasks |P|+|Q| in [%d,%d): %llu tasks, %.3f ms warp time, %.2f us/task\n",
@@ -925,7 +968,6 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
           std::fprintf(stderr, "bit-row tasks W=%d: %llu tasks, %.3f ms warp time, %.2f us/task\n", 1 << (b - 24),
                        hg.hist[0][b], hg.hist[1][b] / 1.965e6, hg.hist[1][b] / 1.965e3 / (double)hg.hist[0][b]);
     }
-    res->roots_out_ms = hg.t_roots_out == ~0ull ? -1.0 : (double)hg.t_roots_out * 1e-6;
     if (cfg.per_root) {
       std::vector<uint64_t> pr(4ull * S.nU);
       CUDA_TRY(cudaMemcpy(pr.data(), W->per_root.p, 32ull * S.nU, cudaMemcpyDeviceToHost));
@@ -963,6 +1005,90 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   }
   res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return MBE_OK;
+}
+
+// ------------------------------------------------------------------ cross-process claim counter
+struct mbe_counter {
+  int device = 0;
+  bool owner = false;  // created here (cudaFree) vs opened from a handle (cudaIpcCloseMemHandle)
+  void* p = nullptr;
+};
+
+int mbe_counter_create(int device, mbe_counter** out) {
+  if (!out) return fail(MBE_EINVAL, "out is NULL");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  mbe_counter* c = new (std::nothrow) mbe_counter();
+  if (!c) return fail(MBE_ENOMEM, "host allocation");
+  c->device = device;
+  c->owner = true;
+  if (cudaMalloc(&c->p, 256) != cudaSuccess || cudaMemset(c->p, 0, 256) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
+    if (c->p) cudaFree(c->p);
+    delete c;
+    return fail(MBE_ECUDA, "claim counter allocation");
+  }
+  *out = c;
+  return MBE_OK;
+}
+
+int mbe_counter_ipc_handle(const mbe_counter* c, void* handle) {
+  if (!c || !handle) return fail(MBE_EINVAL, "NULL argument");
+  if (!c->owner) return fail(MBE_EINVAL, "only the creating process exports the handle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle is 64 bytes");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->p));
+  std::memcpy(handle, &h, 64);
+  return MBE_OK;
+}
+
+int mbe_counter_open(int device, const void* handle, mbe_counter** out) {
+  if (!handle || !out) return fail(MBE_EINVAL, "NULL argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  mbe_counter* c = new (std::nothrow) mbe_counter();
+  if (!c) return fail(MBE_ENOMEM, "host allocation");
+  c->device = device;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  const cudaError_t e = cudaIpcOpenMemHandle(&c->p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return fail(e == cudaErrorDeviceUninitialized ? MBE_EDIST : MBE_ECUDA,
+                std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return MBE_OK;
+}
+
+uint64_t* mbe_counter_ptr(const mbe_counter* c) { return c ? static_cast<uint64_t*>(c->p) : nullptr; }
+
+int mbe_counter_reset(mbe_counter* c, void* stream) {
+  if (!c) return fail(MBE_EINVAL, "NULL counter");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemsetAsync(c->p, 0, 8, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return MBE_OK;
+}
+
+uint64_t mbe_counter_read(mbe_counter* c) {
+  if (!c) return 0;
+  uint64_t v = 0;
+  cudaSetDevice(c->device);
+  if (cudaMemcpy(&v, c->p, 8, cudaMemcpyDeviceToHost) != cudaSuccess) cudaGetLastError();
+  return v;
+}
+
+void mbe_counter_close(mbe_counter* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->owner) cudaFree(c->p);
+  else cudaIpcCloseMemHandle(c->p);
+  delete c;
 }
 
 void mbe_release_workspaces(void) {

@@ -18,6 +18,19 @@
 #define MBE_MINBLOCKS 6
 #endif
 
+// Relocalization / reduction thresholds (build-time tuning constants; result-invariant).
+#define MBE_WIDE_QCAP 256u          // list task -> 8/16-word child if |Q'| <= this ...
+#define MBE_WIDE_RATIO 64u          //   ... or |Q'| <= ratio * |P'| (and <= MBE_WIDE_QMAX)
+#define MBE_WIDE_QMAX 0xffffffffu
+#define MBE_NARROW_QMAX 0u          // same guard for 1/2/4-word children (0 = always relocalize)
+#define MBE_NARROW_RATIO 256u
+#define MBE_AC_MIN 1024u            // list-path children skip the Q' antichain if |Q'| > AC_MIN and > AC_RATIO (|P'|+1)
+#define MBE_AC_RATIO 0xffffffffu
+#define MBE_DEDUP_MIN 512u          // Q' candidate sets above this are deduplicated before the antichain
+#define MBE_DEFER_MIN_DEFAULT 65536u  // default of mbe_config.defer_min
+#define MBE_WIDE_ACMAX 256u         // wide children keep more distinct Q' rows than this unreduced
+#define MBE_WATCHDOG_MS_DEFAULT 120000u
+
 // Immutable device graph after ingest.  Candidate side U is
 // relabelled by ascending (degree, original id): internal id = rank r(v).
 struct DevGraph {
@@ -47,15 +60,23 @@ struct Desc {
 };
 
 struct Globals {
-  unsigned long long root_cursor;
+  // ---- hot prefix: copied back to the host after every launch (MBE_GLOBALS_HOT_BYTES)
+  unsigned long long root_cursor;  // static deal: next local root index
   unsigned int idle;
   unsigned int error;  // 0 ok, 1 arena overflow, 2 depth overflow, 3 internal check, 4 watchdog
   unsigned long long count, hash, tasks, pruned, steals;
+  unsigned long long err_info;
+  unsigned long long claim_state;  // shared counter: (chunks << 33) | (done << 32) | local indices covered
+  unsigned int lpos;               // shared counter: next local root index
+  unsigned int pad0;
+  unsigned long long progress;     // tasks completed / 256 (no-progress watchdog)
+  unsigned long long roots_run;    // level-1 subtrees run by this launch
+  unsigned long long out_records, out_ids;
+  // ---- MBE_STATS and diagnostics (copied back only when requested)
   unsigned long long list_tasks, bitmap_tasks, frames, alg_bytes;
+  unsigned long long alg_list, alg_bitrow, alg_write;  // MBE_STATS: alg_bytes by part
   unsigned int max_depth;
   unsigned int pad;
-  unsigned long long out_records, out_ids;
-  unsigned long long err_info;
   unsigned long long phase[16];  // MBE_STATS: Σ over warps of cycles per phase (see mbe.h)
   unsigned long long max_task[4];  // MBE_STATS: longest single task (cycles): root, list, bit-row, -
   unsigned long long t_roots_out;  // MBE_STATS: ns after launch when the level-1 list ran out
@@ -66,7 +87,11 @@ struct Globals {
   unsigned long long exit_hist[64];  // MBE_STATS diagnostics: warps by exit time (2 ms buckets after launch)
   unsigned long long tl_hist[4][64];  // MBE_STATS diagnostics: cycles by completion time (2 ms buckets): root, list, bit-row tasks, steal+idle
   unsigned long long busy_hist[64];  // MBE_STATS diagnostics: warps registering idle for the first time, by time
+  unsigned long long warp_busy_hist[20];  // MBE_STATS: warps by busy share (Fig. 5 analog), 5 % bins
+  unsigned long long warp_busy_sum, warp_busy_min, warp_busy_max;  // MBE_STATS: task cycles per warp
 };
+#define MBE_GLOBALS_HOT_BYTES 112
+#define MBE_CLAIM_DONE (1ull << 32)
 
 struct SearchParams {
   DevGraph g;
@@ -82,9 +107,11 @@ struct SearchParams {
   uint32_t ac_min, ac_ratio;  // list-path children skip the antichain if |Q'| > ac_min and > ac_ratio*(|P'|+1)   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;
   uint32_t rank, world;
-  unsigned long long* claim_counter;  // NULL -> static deal
+  unsigned long long* claim_counter;  // NULL -> static deal; else shared across ranks (system-scope atomics)
+  unsigned long long* claim_tab;      // [n_roots + 1] chunks claimed by this call: (local base << 32) | global start
+  uint32_t gss_div;                   // chunk = ceil(remaining / gss_div) (guided self-scheduling, 4 * world)
   uint32_t n_warps;
-  unsigned long long watchdog_ns;  // abort (error 4) if a warp idles/waits past this since launch
+  unsigned long long watchdog_ns;  // abort (error 4) when no warp completes a task for this long (0: off)
   // per-warp workspace: region w starts at ws + w * ws_stride (bytes); offsets below are bytes
   uint8_t* ws;
   uint64_t ws_stride;
@@ -115,6 +142,7 @@ struct SearchParams {
 
 // Launches the twin pre-pass and the persistent search kernel on `stream`;
 // ev0/ev1 (cudaEvent_t) bracket the search kernel alone.
+int mbe_launch_twin(const DevGraph& g, int sm_count, void* stream);
 int mbe_launch_search(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0, void* ev1);
 int mbe_launch_search_instr(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0,
                             void* ev1);

@@ -127,7 +127,8 @@ struct Warp {
   uint32_t cur_root;
   bool failed;
   // lane-0 accumulators
-  unsigned long long count, hash, tasks, pruned, steals, list_tasks, bitmap_tasks, frames, alg_bytes;
+  unsigned long long count, hash, tasks, pruned, steals, list_tasks, bitmap_tasks, frames;
+  unsigned long long ab_list, ab_bit, ab_write;  // MBE_STATS algorithmic bytes: list tasks, bit-row tasks, frame writes
   uint32_t max_depth;
 };
 
@@ -1183,7 +1184,9 @@ __device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr
   return prune_frame_wide(Pr, nP, Qr, nQ, W, S, meta, cmask_buf, lane, prof);
 }
 
-// Account the nP tasks of a child frame decided at build time (nS survive the check).
+// Account the nP tasks of a child frame decided at build time (nS survive the check).  Algorithmic
+// bytes (bit-row path): every task reads row(x) and every row of its frame, i.e.
+// 4 W (1 + |P| + |Q|) with |Q| the frame's R1-reduced Q rows (nQ).
 __device__ __forceinline__ void account_children(Warp& w, const SearchParams& p, uint32_t nP, uint32_t nS,
                                                  uint32_t W, uint32_t nQ) {
   if (w.lane == 0) {
@@ -1195,9 +1198,17 @@ __device__ __forceinline__ void account_children(Warp& w, const SearchParams& p,
     }
     if (MBE_STATS_ON) {
       w.bitmap_tasks += nP;
-      w.alg_bytes += (unsigned long long)nP * (4ull * W * (1ull + nP + nQ) + 4ull * nP);
+      w.ab_bit += (unsigned long long)nP * 4ull * W * (1ull + nP + nQ);
     }
   }
+}
+
+// MBE_STATS only: size of the R1-reduced Q' of a child whose tasks were all decided on the raw
+// candidate rows (no frame stored), so its tasks are charged the rows the frame would hold.
+__device__ __noinline__ uint32_t stats_r1_size(uint32_t Wn, const uint32_t* src, uint32_t n, Warp& w,
+                                               const SearchParams& p) {
+  if (n == 0 || (uint64_t)n * Wn > 4ull * p.skey2_off) return n;
+  return antichain_w(Wn, src, n, reinterpret_cast<uint32_t*>(w.skey), false, w.lane, w.sm);
 }
 
 // ================================================================== list path
@@ -1453,7 +1464,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   if (lane == 0 && MBE_STATS_ON) {
     w.list_tasks++;
     // N(x) + reverse-scan adjacency incl. offsets + touched rows (+ frame L, P, R reads)
-    w.alg_bytes += 4ull * dx + 4ull * (visits + nLp) + 8ull * nt + 4ull * (nL + 2ull * nP + nR);
+    w.ab_list += 4ull * dx + 4ull * (visits + nLp) + 8ull * nt + 4ull * (nL + 2ull * nP + nR);
   }
   if (nonmax) return;
 
@@ -1561,7 +1572,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       C[4] = nRp;
       C[5] = w.cur_root;
       *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-      if MBE_STATS_ON w.alg_bytes += 4ull * size;
+      if MBE_STATS_ON w.ab_write += 4ull * size;
     }
     publish_frame(w, p, size, nT);
   }
@@ -1705,9 +1716,12 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
       }
     }
     account_task(w, p, dom);
-    if (lane == 0 && MBE_STATS_ON) {
-      w.bitmap_tasks++;
-      w.alg_bytes += 4ull * Wn * (1ull + nQc);
+    if MBE_STATS_ON {
+      const uint32_t q1 = stats_r1_size(Wn, qbuf, nQc, w, p);
+      if (lane == 0) {
+        w.bitmap_tasks++;
+        w.ab_bit += 4ull * Wn * (2ull + q1);
+      }
     }
     if (!dom) {
       unsigned long long sL2 = 0;
@@ -1745,8 +1759,8 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
                       : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
                                 : prune_frame<4>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane);
   MBE_PHASE(15, tph);
-  account_children(w, p, nPc, nS, Wn, nQc);
   if (nS == 0) {
+    account_children(w, p, nPc, 0, Wn, MBE_STATS_ON ? stats_r1_size(Wn, qbuf, nQc, w, p) : 0u);
     MBE_PHASE(14, tph);
     return;
   }
@@ -1776,6 +1790,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   } else {
     nQk = antichain_w(Wn, qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
   }
+  account_children(w, p, nPc, nS, Wn, nQk);
   uint32_t* S = CQ + (size_t)nQk * Wn;
   for (uint32_t t = lane; t < nS; t += 32) S[t] = Stmp[t];
   uint64_t size = (uint64_t)(S + nS - C);
@@ -1787,7 +1802,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if MBE_STATS_ON w.alg_bytes += 4ull * size;
+    if MBE_STATS_ON w.ab_write += 4ull * size;
   }
   publish_frame(w, p, size, nS);
   MBE_PHASE(14, tph);
@@ -1834,7 +1849,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     account_task(w, p, dom);
     if (lane == 0 && MBE_STATS_ON) {
       w.bitmap_tasks++;
-      w.alg_bytes += 4ull * W * (1ull + nQ + i);
+      w.ab_bit += 4ull * W * (1ull + nP + nQ);
     }
     if (dom) return;
   }
@@ -1950,12 +1965,13 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, w.pbuf, lane);
   MBE_PHASE(15, tph);
   wide_sub(30);
-  account_children(w, p, nPc, nS, Wn, nQc);
   if (nS == 0) {
+    account_children(w, p, nPc, 0, Wn, MBE_STATS_ON ? stats_r1_size(Wn, scratch, nQc, w, p) : 0u);
     MBE_PHASE(14, tph);
     return;
   }
   const uint32_t nQk = antichain_w(Wn, scratch, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+  account_children(w, p, nPc, nS, Wn, nQk);
   wide_sub(31);
   uint32_t* S = CQ + (size_t)nQk * Wn;
   for (uint32_t t = lane; t < nS; t += 32) S[t] = Stmp[t];
@@ -1968,7 +1984,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if MBE_STATS_ON w.alg_bytes += 4ull * size;
+    if MBE_STATS_ON w.ab_write += 4ull * size;
   }
   publish_frame(w, p, size, nS);
   MBE_PHASE(14, tph);
@@ -2092,6 +2108,73 @@ __device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const 
   return false;
 }
 
+// ================================================================== level-1 subtree claims
+// Dynamic claiming through a counter shared by every rank ("subtree fetching", lifted to a
+// box-wide counter).  The warps of this launch draw LOCAL indices 0, 1, 2, ... from
+// gl->lpos; local indices map onto chunks of global root positions that this launch claimed from the
+// shared counter with ONE system-scope atomic per chunk (guided self-scheduling: a chunk is
+// ceil(remaining / gss_div) positions, so chunks shrink as the list drains).  The chunk table
+// (claim_tab, entries (local base << 32) | global start, appended in order) is published through
+// gl->claim_state = (chunks << 33) | (done << 32) | local indices covered.  The warp whose local index
+// equals the covered count is the only one that claims the next chunk; warps beyond it wait for the
+// publication.  The table doubles as the claim log: a relaunch after an arena overflow starts with the
+// previous launch's claim_state, so it replays exactly the chunks this call already took.
+// Lane 0 only.  Returns the global root position, or ~0u when this rank has no more.
+__device__ __noinline__ uint32_t claim_root_shared(const SearchParams& p) {
+  const uint32_t i = atomicAdd(&p.gl->lpos, 1u);
+  const uint32_t n = p.g.n_roots;
+  for (;;) {
+    const unsigned long long s = ld_volatile64(&p.gl->claim_state);
+    const uint32_t known = (uint32_t)s;
+    const uint32_t nch = (uint32_t)(s >> 33);
+    if (i < known) {  // last chunk whose local base <= i
+      uint32_t lo = 0, hi = nch;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint32_t)(ld_volatile64(&p.claim_tab[mid]) >> 32) <= i) lo = mid;
+        else hi = mid;
+      }
+      const unsigned long long e = ld_volatile64(&p.claim_tab[lo]);
+      return (uint32_t)e + (i - (uint32_t)(e >> 32));
+    }
+    if (s & MBE_CLAIM_DONE) return ~0u;
+    if (i == known) {  // this warp claims the next chunk for the launch
+      const unsigned long long g0 = *(volatile unsigned long long*)p.claim_counter;
+      unsigned long long pos = ~0ull, len = 0;
+      if (g0 < n) {
+        const unsigned long long rem = n - g0;
+        const unsigned long long c = (rem + p.gss_div - 1) / p.gss_div;
+        pos = atomicAdd_system(p.claim_counter, c);
+        if (pos < n) len = min(c, (unsigned long long)n - pos);
+      }
+      if (len == 0) {
+        atomicExch(&p.gl->claim_state, s | MBE_CLAIM_DONE);
+        return ~0u;
+      }
+      p.claim_tab[nch] = ((unsigned long long)known << 32) | pos;
+      __threadfence();
+      atomicExch(&p.gl->claim_state, ((unsigned long long)(nch + 1) << 33) | (known + len));
+      continue;
+    }
+    __nanosleep(128);  // another warp is claiming the chunk that covers i
+  }
+}
+
+// No-progress watchdog (lane 0): true once no warp has completed a task for p.watchdog_ns.
+struct Watch {
+  unsigned long long seen, since;
+};
+__device__ __forceinline__ bool watchdog_expired(const SearchParams& p, Watch& wd) {
+  if (p.watchdog_ns == 0) return false;
+  const unsigned long long pr = ld_volatile64(&p.gl->progress), now = globaltimer_ns();
+  if (pr != wd.seen) {
+    wd.seen = pr;
+    wd.since = now;
+    return false;
+  }
+  return now - wd.since > p.watchdog_ns;
+}
+
 // ================================================================== kernel
 __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(SearchParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2123,7 +2206,8 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
   w.cur_root = 0;
   w.failed = false;
   w.count = w.hash = w.tasks = w.pruned = w.steals = 0;
-  w.list_tasks = w.bitmap_tasks = w.frames = w.alg_bytes = 0;
+  w.list_tasks = w.bitmap_tasks = w.frames = 0;
+  w.ab_list = w.ab_bit = w.ab_write = 0;
   w.max_depth = 0;
   if (lane == 0) {
     for (int k = 0; k < 16; ++k) w.sm->ph[k] = 0;
@@ -2133,6 +2217,10 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
 
   const bool steal = !(p.flags & F_NO_STEAL);
   const unsigned long long t_start = globaltimer_ns();
+  const unsigned long long c_start = (unsigned long long)clock64();
+  Watch wd{~0ull, t_start};
+  uint32_t done_tasks = 0;
+  unsigned long long roots = 0;
   bool roots_done = false;
   bool registered = false;
   bool ever_idle = false;
@@ -2180,7 +2268,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         // exhausted: wait for thieves still reading it, then pop
         if (lane == 0) {
           while (ld_volatile(&dsc->done) < nP - w.sm->ffirst[d]) {
-            if (ld_volatile(&p.gl->error) || globaltimer_ns() - t_start > p.watchdog_ns) {
+            if (ld_volatile(&p.gl->error) || watchdog_expired(p, wd)) {
               set_error(p, 4u, 1ull);
               w.failed = true;
               break;
@@ -2222,8 +2310,12 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       // ---- empty stack: next level-1 subtree (coarse-grained task)
       unsigned long long pos = 0;
       if (lane == 0) {
-        if (p.claim_counter) pos = atomicAdd(p.claim_counter, 1ull);
-        else pos = atomicAdd(&p.gl->root_cursor, 1ull) * p.world + p.rank;
+        if (p.claim_counter) {
+          const uint32_t q = claim_root_shared(p);
+          pos = q == ~0u ? ~0ull : q;
+        } else {
+          pos = atomicAdd(&p.gl->root_cursor, 1ull) * p.world + p.rank;
+        }
       }
       pos = __shfl_sync(FULLMASK, pos, 0);
       if (pos >= p.g.n_roots) {
@@ -2233,6 +2325,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       }
       xr = p.g.root_order[pos];
       kind = 2;
+      ++roots;
     } else {
       // ---- idle: register, then steal single tasks or terminate
       if (!registered) {
@@ -2245,8 +2338,8 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       uint32_t stop = 0;
       if (lane == 0) {
         stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
-        if (!stop && globaltimer_ns() - t_start > p.watchdog_ns) {
-          set_error(p, 4u, 0ull);  // watchdog: never hang the device
+        if (!stop && watchdog_expired(p, wd)) {
+          set_error(p, 4u, 0ull);  // no-progress watchdog: never hang the device
           stop = 1;
         }
       }
@@ -2304,6 +2397,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
 
     __syncwarp();
     if (lane == 0) {
+      if ((++done_tasks & 255u) == 0u) atomicAdd(&p.gl->progress, 1ull);  // watchdog heartbeat
       if (kind != 2) atomicAdd(&dsc->done, 1u);
       if (kind == 1 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
       if (kind == 3) w.steals++;
@@ -2335,11 +2429,22 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
     atomicAdd(&p.gl->tasks, w.tasks);
     atomicAdd(&p.gl->pruned, w.pruned);
     atomicAdd(&p.gl->steals, w.steals);
+    if (roots) atomicAdd(&p.gl->roots_run, roots);
     if MBE_STATS_ON {
+      // per-warp workload distribution (Fig. 5 analog): task cycles vs cycles until this warp exits
+      const unsigned long long busy = w.sm->ph[0] + w.sm->ph[1] + w.sm->ph[2];
+      const unsigned long long total = max(1ull, (unsigned long long)clock64() - c_start);
+      atomicAdd(&p.gl->warp_busy_hist[min(19ull, busy * 20ull / total)], 1ull);
+      atomicAdd(&p.gl->warp_busy_sum, busy);
+      atomicMin(&p.gl->warp_busy_min, busy);
+      atomicMax(&p.gl->warp_busy_max, busy);
       atomicAdd(&p.gl->list_tasks, w.list_tasks);
       atomicAdd(&p.gl->bitmap_tasks, w.bitmap_tasks);
       atomicAdd(&p.gl->frames, w.frames);
-      atomicAdd(&p.gl->alg_bytes, w.alg_bytes);
+      atomicAdd(&p.gl->alg_bytes, w.ab_list + w.ab_bit + w.ab_write);
+      atomicAdd(&p.gl->alg_list, w.ab_list);
+      atomicAdd(&p.gl->alg_bitrow, w.ab_bit);
+      atomicAdd(&p.gl->alg_write, w.ab_write);
       atomicMax(&p.gl->max_depth, w.max_depth);
       for (int k = 0; k < 16; ++k) atomicAdd(&p.gl->phase[k], w.sm->ph[k]);
     }
@@ -2422,10 +2527,6 @@ int MBE_EXPORT(mbe_search_max_ctas_per_sm)(int block, int smem_bytes) {
 int MBE_EXPORT(mbe_launch_search)(const SearchParams& p, int grid, int block, int smem_bytes, void* stream, void* ev0,
                                    void* ev1) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!(p.flags & F_NO_TWIN)) {
-    mbe_twin_kernel<<<148 * 8, 256, 0, s>>>(p.g, const_cast<uint8_t*>(p.g.twin));
-    if (cudaGetLastError() != cudaSuccess) return -1;
-  }
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(mbe_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
@@ -2434,7 +2535,20 @@ int MBE_EXPORT(mbe_launch_search)(const SearchParams& p, int grid, int block, in
     attr_set = true;
   }
   if (cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev0), s) != cudaSuccess) return -1;
-  mbe_search_kernel<<<grid, block, smem_bytes, s>>>(p);
-  if (cudaGetLastError() != cudaSuccess) return -1;
+  // Cooperative launch: the runtime refuses (instead of deadlocking) when the persistent grid cannot be
+  // co-resident, which the idle-count termination requires.
+  SearchParams arg = p;
+  void* args[] = {&arg};
+  if (cudaLaunchCooperativeKernel((const void*)mbe_search_kernel, dim3(grid), dim3(block), args, (size_t)smem_bytes, s) !=
+      cudaSuccess)
+    return -1;
   return cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev1), s) == cudaSuccess ? 0 : -1;
 }
+
+#if !MBE_INSTR
+// Root twin flags (graph-only; computed once per loaded side), grid = SMs x 8 CTAs of 8 warps.
+int mbe_launch_twin(const DevGraph& g, int sm_count, void* stream) {
+  mbe_twin_kernel<<<sm_count * 8, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(g, const_cast<uint8_t*>(g.twin));
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+#endif

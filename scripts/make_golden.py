@@ -19,10 +19,25 @@ import oracle  # noqa: E402
 from paper_2401_05039_b200 import inputs as I  # noqa: E402
 
 PATH = os.path.join(ROOT, "tests", "golden", "configs.txt")
-HEADER = """# Oracle results on the full-size synthetic configs (SURVEY.md §8(d), BASELINE.json configs[1..4]).
-# Written by scripts/make_golden.py, which calls only oracle/ (plain Algorithm 1, P:118-169) on the
-# graphs of paper_2401_05039_b200/inputs.py.  Columns: config count hash tasks pruned oracle_seconds threads host
+HEADER = """# Oracle results on the full-size synthetic configs (SURVEY.md §8(d), BASELINE.json configs[1..4]; C5p =
+# C5 with planted communities, inputs.CONFIGS).  Written by scripts/make_golden.py, which calls only
+# oracle/ (plain Algorithm 1, P:118-169) on the graphs of paper_2401_05039_b200/inputs.py.
+# Columns: config count hash tasks pruned oracle_seconds threads host[:cpu-model]
+# Rows with host "vm" and 16 threads (C2, C3, C5) were timed in round 1 on a GPU box's host (the dev
+# container has 8 cores); rows with 8 threads on the 8-core dev container.
 """
+
+
+def host_tag() -> str:
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return platform.node() + (":" + "-".join(model.replace("(R)", "").split()) if model else "")
 
 
 def main():
@@ -42,7 +57,7 @@ def main():
         t = time.time()
         r = oracle.mbea(g, threads=a.threads)
         dt = time.time() - t
-        rows[c] = f"{c} {r.count} {r.hash:#018x} {r.tasks} {r.pruned} {dt:.1f} {r.threads} {platform.node()}"
+        rows[c] = f"{c} {r.count} {r.hash:#018x} {r.tasks} {r.pruned} {dt:.1f} {r.threads} {host_tag()}"
         print(rows[c], flush=True)
         with open(out, "w") as f:
             f.write(HEADER)

@@ -11,8 +11,8 @@ import pytest
 
 import oracle
 from oracle import reference as R
-from paper_2401_05039_b200 import (MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN, MBE_STATS, MBE_STEAL_HALF, MBE_STEAL_ONE,
-                                   MBEGraph)
+from paper_2401_05039_b200 import (MBE_ARENA_GROW, MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN, MBE_STATS, MBE_STEAL_HALF,
+                                   MBE_STEAL_ONE, ClaimCounter, MBEError, MBEGraph)
 from paper_2401_05039_b200 import inputs as I
 
 pytestmark = pytest.mark.gpu
@@ -130,15 +130,15 @@ def test_wide_bit_rows(g, T):
 
 @pytest.mark.parametrize("g", [I.random_bipartite(12, 400, 0.7, 1), I.random_bipartite(40, 700, 0.3, 4),
                                I.random_bipartite(30, 500, 0.5, 6)], ids=lambda g: g.name)
-@pytest.mark.parametrize("defer_min", ["1", "64"])
-def test_deferred_step3_on_wide_children(g, defer_min, monkeypatch):
-    """MBE_DEFER_MIN forces large wide list-path children to publish every task unchecked (each task
-    runs Step 3 itself): same tree (tasks, pruned) and result as the eager frame-build check."""
+@pytest.mark.parametrize("defer_min", [1, 64])
+def test_deferred_step3_on_wide_children(g, defer_min):
+    """mbe_config.defer_min forces large wide list-path children to publish every task unchecked (each
+    task runs Step 3 itself): same tree (tasks, pruned) and result as the eager frame-build check."""
     want = oracle.mbea(g)
-    monkeypatch.setenv("MBE_DEFER_MIN", defer_min)
-    assert same(gpu(g), want)
-    assert same(gpu(g, flags=MBE_STATS), want)
-    assert same(gpu(g, flags=MBE_STEAL_HALF), want)
+    assert same(gpu(g, defer_min=defer_min), want)
+    assert same(gpu(g, defer_min=defer_min, flags=MBE_STATS), want)
+    assert same(gpu(g, defer_min=defer_min, flags=MBE_STEAL_HALF), want)
+    assert same(gpu(g, defer_min=0xFFFFFFFF), want)
 
 
 @pytest.mark.parametrize("ctas,threads", [(1, 32), (1, 128), (2, 128), (4, 64)])
@@ -216,12 +216,11 @@ def test_metamorphic_transpose_isolated_duplicates():
     assert (gpu(gd).count, gpu(gd).hash) == (base.count, base.hash)
 
 
-@pytest.mark.parametrize("threads", ["1", "3", "16"])
-def test_parallel_ingest_unsorted_duplicate_rows(threads, monkeypatch):
-    """Host ingest split over threads (edge-balanced ranges; MBE_INGEST_THREADS forces the split on a
-    small graph): rows given unsorted with duplicates, empty rows and columns -> the oracle's result on
-    the deduplicated graph (reading Z8), for both candidate sides."""
-    monkeypatch.setenv("MBE_INGEST_THREADS", threads)
+@pytest.mark.parametrize("threads", [1, 3, 16])
+def test_parallel_ingest_unsorted_duplicate_rows(threads):
+    """Host ingest split over threads (edge-balanced ranges; mbe_load_csr flags bits 0-7 force the split
+    on a small graph): rows given unsorted with duplicates, empty rows and columns -> the oracle's result
+    on the deduplicated graph (reading Z8), for both candidate sides."""
     g = I.erdos_renyi_c1b(160, 120)
     e = g.edges()
     rng = np.random.default_rng(5)
@@ -233,7 +232,7 @@ def test_parallel_ingest_unsorted_duplicate_rows(threads, monkeypatch):
     row_ptr = np.zeros(n1 + 1, dtype=np.uint64)
     row_ptr[1:] = np.cumsum(np.bincount(rows, minlength=n1)).astype(np.uint64)
     want = oracle.mbea(I.from_edges(n1, n2, e[:, 0], e[:, 1]))
-    with MBEGraph(n1, n2, row_ptr, cols.astype(np.uint32)) as G:
+    with MBEGraph(n1, n2, row_ptr, cols.astype(np.uint32), ingest_threads=threads) as G:
         assert G.info()["n_edges"] == len(e)
         for side in (1, 2):
             r = G.enumerate(candidate_side=side)
@@ -267,29 +266,93 @@ def test_rank_shares_sum_to_whole(world):
 
 
 def test_shared_claim_counter_logical_ranks():
-    """Dynamic claiming through one device counter shared by 2 logical ranks (one GPU)."""
-    import threading
+    """Dynamic claiming through one shared counter by 2 logical ranks of one process, run one after the
+    other (each persistent launch owns the whole GPU): the shares sum to the whole, and the first rank
+    drains the counter in guided-self-scheduling chunks."""
+    g = I.random_bipartite(400, 300, 0.03, 10)
+    want = oracle.mbea(g)
+    ctr = ClaimCounter(0)
+    outs = []
+    for k in range(2):
+        with MBEGraph.from_graph(g) as G:
+            outs.append(G.enumerate(rank=k, world=2, claim_counter=ctr.ptr))
+    n_roots = int((np.diff(g.row_ptr) > 0).sum()) if g.n1 <= g.n2 else int((np.bincount(g.col_idx, minlength=g.n2) > 0).sum())
+    assert outs[0].roots_claimed + outs[1].roots_claimed == n_roots
+    assert outs[0].claim_chunks >= 2
+    assert ctr.read() >= n_roots
+    assert sum(o.count for o in outs) == want.count
+    assert sum(o.hash for o in outs) & R.MASK64 == want.hash
+    assert sum(o.tasks for o in outs) == want.tasks
+    ctr.close()
 
-    import torch
+
+def test_shared_counter_overflow_relaunch_replays_claims():
+    """an arena-overflow relaunch must replay exactly the chunks this call claimed from
+    the shared counter.  A 4 KiB initial arena with MBE_ARENA_GROW overflows, relaunches, and the result
+    is still the whole (one rank) / the exact share."""
+    g = I.random_bipartite(300, 260, 0.05, 3)
+    want = oracle.mbea(g)
+    ctr = ClaimCounter(0)
+    with MBEGraph.from_graph(g) as G:
+        r = G.enumerate(claim_counter=ctr.ptr, arena_bytes=4096, flags=MBE_ARENA_GROW)
+        assert r.attempts > 1
+        assert same(r, want)
+        ctr.reset()
+        r0 = G.enumerate(rank=0, world=2, claim_counter=ctr.ptr, arena_bytes=4096, flags=MBE_ARENA_GROW)
+        r1 = G.enumerate(rank=1, world=2, claim_counter=ctr.ptr, arena_bytes=4096, flags=MBE_ARENA_GROW)
+        assert r0.attempts > 1
+        assert (r0.count + r1.count, (r0.hash + r1.hash) & R.MASK64) == (want.count, want.hash)
+        assert r0.tasks + r1.tasks == want.tasks
+        with pytest.raises(MBEError) as e:  # fixed arena: overflow is an error, never a partial count
+            G.enumerate(arena_bytes=4096)
+        assert e.value.code == -4
+    ctr.close()
+
+
+def _ipc_rank(rank, world, handle_q, out_q):
+    import numpy as np  # noqa: F811
+
+    from paper_2401_05039_b200 import ClaimCounter, MBEGraph
+    from paper_2401_05039_b200 import inputs as I
+
+    g = I.random_bipartite(400, 300, 0.03, 10)
+    if rank == 0:
+        ctr = ClaimCounter(0)
+        for _ in range(world - 1):
+            handle_q.put(ctr.ipc_handle())
+    else:
+        ctr = ClaimCounter(0, handle=handle_q.get(timeout=120))
+    with MBEGraph.from_graph(g) as G:
+        r = G.enumerate(rank=rank, world=world, claim_counter=ctr.ptr)
+    out_q.put((rank, r.count, r.hash, r.tasks, r.roots_claimed))
+    if rank == 0:
+        out_q.put(("done-wait",))
+        import time
+        time.sleep(3)  # keep the counter alive while the other rank may still use it
+    ctr.close()
+
+
+def test_claim_counter_ipc_two_processes_one_gpu():
+    """Two PROCESSES share rank 0's counter through its CUDA IPC handle (same GPU here; peer GPUs over
+    NVLink in a real box): their shares sum to the oracle's whole."""
+    import multiprocessing as mp
 
     g = I.random_bipartite(400, 300, 0.03, 10)
     want = oracle.mbea(g)
-    ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
-    Gs = [MBEGraph.from_graph(g) for _ in range(2)]
-    streams = [torch.cuda.Stream() for _ in range(2)]
-    out = [None, None]
-
-    def run(k):
-        out[k] = Gs[k].enumerate(rank=k, world=2, claim_counter=ctr.data_ptr(), stream=streams[k].cuda_stream)
-
-    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
-    [t.start() for t in th]
-    [t.join() for t in th]
-    for G in Gs:
-        G.close()
-    assert out[0].count + out[1].count == want.count
-    assert (out[0].hash + out[1].hash) & R.MASK64 == want.hash
-    assert out[0].tasks + out[1].tasks == want.tasks
+    ctx = mp.get_context("spawn")
+    hq, oq = ctx.Queue(), ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, hq, oq)) for r in range(2)]
+    [p.start() for p in procs]
+    res = {}
+    while len(res) < 2:
+        item = oq.get(timeout=300)
+        if item[0] != "done-wait":
+            res[item[0]] = item[1:]
+    [p.join(120) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    assert res[0][0] + res[1][0] == want.count
+    assert (res[0][1] + res[1][1]) & R.MASK64 == want.hash
+    assert res[0][2] + res[1][2] == want.tasks
 
 
 # ------------------------------------------------------------------ full-size configs
@@ -304,7 +367,7 @@ def _golden_configs():
     return rows
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C5p"])
 def test_full_config_matches_oracle_golden(cfg):
     gold = _golden_configs()
     if cfg not in gold:
@@ -314,7 +377,7 @@ def test_full_config_matches_oracle_golden(cfg):
     assert (r.count, r.hash, r.tasks, r.pruned) == gold[cfg]
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5", "C5p"])
 def test_full_config_sampled_roots_vs_oracle(cfg):
     """At full size, in the bench launch configuration: per level-1 subtree results for a seeded
     sample of roots (the heaviest by degree plus uniform ones) equal the oracle's, computed one by one."""
