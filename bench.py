@@ -146,24 +146,35 @@ def oracle_rate(g, target_s: float, seed: int = 7, config: str = ""):
     rng = np.random.default_rng(seed)
 
     def run(k):
+        import resource
+
         m = max(1, len(roots) // k)
         pick = np.sort(rng.choice(len(roots), size=m, replace=False))
+        ru0 = resource.getrusage(resource.RUSAGE_SELF)
         t0 = time.perf_counter()
         pr = oracle.mbea_roots(g, roots[pick], candidate_side=side)
-        return int(pr[:, 0].sum()), time.perf_counter() - t0, m
+        wall = time.perf_counter() - t0
+        ru1 = resource.getrusage(resource.RUSAGE_SELF)
+        cpu_s = (ru1.ru_utime - ru0.ru_utime) + (ru1.ru_stime - ru0.ru_stime)
+        return int(pr[:, 0].sum()), wall, m, cpu_s
 
     full = golden_full_run(config)
     if full:
         k = max(1, int(round(full["seconds"] * full["threads"] / threads / target_s)))
     else:
         k = max(1, len(roots) // 64)
-        _, dt, _ = run(k)
-        k = max(1, int(round(k * dt / target_s)))
-    cnt, dt, m = run(k)
+        _, _, _, c0 = run(k)
+        k = max(1, int(round(k * c0 / threads / target_s)))
+    cnt, dt, m, cpu_s = run(k)
+    # rate = count / (thread-seconds / threads): the sample's work spread evenly over the host's cores, as the
+    # full run (96K subtrees over the same cores) spreads it; a small sample cannot balance its heaviest
+    # subtree (up to minutes on one thread), so its wall time alone would understate the CPU
+    eff = max(cpu_s / threads, 1e-9)
     sample = (f"seeded uniform random {m} of the {len(roots)} level-1 subtrees (1/{k}, no exclusion: unbiased for the "
-              f"full-run rate), {cnt} bicliques in {dt:.1f} s on {threads} threads")
-    return cnt / dt, dict(count=cnt, seconds=dt, roots=m, frac=m / max(1, len(roots)), threads=threads, side=side,
-                          k=k, sample=sample)
+              f"full-run work), {cnt} bicliques, {cpu_s:.1f} thread-s on {threads} threads ({dt:.1f} s wall); "
+              f"rate = count / (thread-s / threads)")
+    return cnt / eff, dict(count=cnt, seconds=eff, wall_s=dt, cpu_s=cpu_s, roots=m, frac=m / max(1, len(roots)),
+                           threads=threads, side=side, k=k, sample=sample)
 
 
 def golden_full_run(config):
@@ -187,7 +198,7 @@ def run_reference(args):
 
     oracle.build_oracle()
     g = graph_of(args.config)
-    per_step_target = max(5.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step_target = max(2.0, min(15.0, 60.0 / max(1, args.steps + args.warmup)))
     rates, infos = [], []
     for s in range(args.warmup + args.steps):
         r, info = oracle_rate(g, per_step_target, seed=7 + s, config=args.config)
@@ -468,7 +479,7 @@ def main():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--T", type=int, default=0)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--static-deal", action="store_true", help="multi-rank: deal level-1 subtrees k = rank mod N")
     args = ap.parse_args()

@@ -712,10 +712,11 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   const uint32_t ctas_per_sm = std::min<uint32_t>(cfg.ctas_per_sm ? cfg.ctas_per_sm : (uint32_t)MBE_MINBLOCKS, (uint32_t)occ);
   const uint32_t grid = (uint32_t)g->sm_count * ctas_per_sm;
   const uint32_t n_warps = grid * (threads / 32);
-  // auto arena: proportional to the graph, 256 KiB .. 8 MiB per warp; grown x4 and relaunched on overflow
+  // auto arena: proportional to the graph, 256 KiB .. 2 MiB per warp (high-water marks: C2 0.32, C3 0.48,
+  // C5 0.60, C4 0.91 MB); grown x4 and relaunched on overflow
   const bool grow = cfg.arena_bytes == 0 || (cfg.flags & MBE_ARENA_GROW);
   uint64_t arena = cfg.arena_bytes ? cfg.arena_bytes
-                                   : std::min<uint64_t>(8ull << 20, std::max<uint64_t>(256ull << 10, 16ull * (S.nU + S.nV + g->nE)));
+                                   : std::min<uint64_t>(2ull << 20, std::max<uint64_t>(256ull << 10, 16ull * (S.nU + S.nV + g->nE)));
   arena = (arena + 255) & ~255ull;
   // auto bit-row threshold: the widest rows (512 columns) whose workspace fits in 80% of free memory
   // (decided once per loaded side; the free-memory query is not repeated on every call)
@@ -739,7 +740,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     }
     S.auto_T = T;
   }
-  const uint32_t wmax = mbe_words_for(T);
+  const bool auto_T = cfg.bitmap_threshold == 0;
+  uint32_t wmax = mbe_words_for(T);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cfg.stream);
   static const bool dbg_timing = std::getenv("MBE_DEBUG_TIMING") != nullptr;
   static const bool dbg_longest = std::getenv("MBE_DEBUG_LONGEST") != nullptr;
@@ -799,6 +801,12 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     const auto tw0 = std::chrono::steady_clock::now();
     if (!wg.w) {
       rc = checkout_workspace(g->device, n_warps, S.nU, S.maxdegU, arena, wmax, &wg.w);
+      // auto threshold: narrower rows when the device is shared (e.g. several ranks on one GPU)
+      while (rc == MBE_ENOMEM && auto_T && T > 128) {
+        T /= 2;
+        wmax = mbe_words_for(T);
+        rc = checkout_workspace(g->device, n_warps, S.nU, S.maxdegU, arena, wmax, &wg.w);
+      }
       if (rc) return rc;
     }
     Workspace* W = wg.w;
@@ -963,6 +971,16 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
         if (hg.hist[0][b])
           std::fprintf(stderr, "wide child build, %s: %llu calls, %.3f ms warp time, %.2f us/call\n", sub[b - 29],
                        hg.hist[0][b], hg.hist[1][b] / 1.965e6, hg.hist[1][b] / 1.965e3 / (double)hg.hist[0][b]);
+      std::fprintf(stderr, "max arena words per warp: %llu (%.2f MB)\n", hg.max_arena_words, hg.max_arena_words * 4e-6);
+      for (int b = 0; b < 12; ++b)
+        if (hg.list_nt_hist[0][b])
+          std::fprintf(stderr, "list tasks touched in [4^%d, 4^%d): %llu tasks, %.3f ms warp time\n", b, b + 1,
+                       hg.list_nt_hist[0][b], hg.list_nt_hist[1][b] / 1.965e6);
+      for (int k = 0; k < 2; ++k)
+        for (int b = 0; b < 8; ++b)
+          if (hg.wide_hist[2 * k][b])
+            std::fprintf(stderr, "wide tasks %s in [4^%d, 4^%d): %llu tasks, %.3f ms warp time\n", k ? "|P|" : "|Q|", b,
+                         b + 1, hg.wide_hist[2 * k][b], hg.wide_hist[2 * k + 1][b] / 1.965e6);
       for (int b = 24; b < 29; ++b)
         if (hg.hist[0][b])
           std::fprintf(stderr, "bit-row tasks W=%d: %llu tasks, %.3f ms warp time, %.2f us/task\n", 1 << (b - 24),

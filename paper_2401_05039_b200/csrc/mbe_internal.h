@@ -7,15 +7,18 @@
 #define MBE_WMAX 16        // bit rows of up to 16 x 32 = 512 columns
 #define MBE_SLOT_WORDS 8   // per-vertex scratch slot: count, -, tag (2), bit row words 0-3 = one 32-B sector
 #define MBE_SEXT_WORDS 12  // per-vertex extension: bit row words 4-15 (wide rows only)
-#define MBE_SMEM_SORT 256  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
+#ifndef MBE_SMEM_SORT
+#define MBE_SMEM_SORT 128  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
+#endif
 #define MBE_HDR_WORDS 8    // frame header
-// Persistent launch shape: 128-thread CTAs, 6 per SM (85 registers/thread, 24 warps/SM: more
-// warps in flight beat fewer spills on this latency-bound search).
+// Persistent launch shape: 128-thread CTAs, 7 per SM (72 registers/thread, 28 warps/SM, 6.6 KB of
+// shared memory per warp): on C4/C5 7 CTAs beat 6 (85 registers) by 4-5 % and 8 (64 registers,
+// spills) lost 30 % on C4 (profiles/ab_r2_occupancy.jsonl).
 #ifndef MBE_BLOCK
 #define MBE_BLOCK 128
 #endif
 #ifndef MBE_MINBLOCKS
-#define MBE_MINBLOCKS 6
+#define MBE_MINBLOCKS 7
 #endif
 
 // Relocalization / reduction thresholds (build-time tuning constants; result-invariant).
@@ -89,6 +92,9 @@ struct Globals {
   unsigned long long busy_hist[64];  // MBE_STATS diagnostics: warps registering idle for the first time, by time
   unsigned long long warp_busy_hist[20];  // MBE_STATS: warps by busy share (Fig. 5 analog), 5 % bins
   unsigned long long warp_busy_sum, warp_busy_min, warp_busy_max;  // MBE_STATS: task cycles per warp
+  unsigned long long max_arena_words;  // MBE_STATS: high-water mark of one warp's arena (words)
+  unsigned long long list_nt_hist[2][12];  // MBE_STATS diagnostics: list tasks by touched vertices (log4 buckets): count, cycles
+  unsigned long long wide_hist[4][8];  // MBE_STATS diagnostics: wide tasks: [0] by log2(nQ) count, [1] cycles, [2] by log2(nP) count, [3] cycles
 };
 #define MBE_GLOBALS_HOT_BYTES 112
 #define MBE_CLAIM_DONE (1ull << 32)

@@ -62,6 +62,9 @@
 #ifndef MBE_CLS_MLP
 #define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification (2 -> 4: C5 80 -> 68 ms)
 #endif
+#ifndef MBE_DEBUG_DELAYS
+#define MBE_DEBUG_DELAYS 0  // 1: random __nanosleep at the claim / steal / publish / pop points (race stress builds)
+#endif
 #define KIND_LIST 0u
 #define KIND_BITMAP 1u
 #define HDR_UNCHECKED (1u << 16)  // frame header flag: Step 3 not yet run for its tasks (each task runs it)
@@ -69,10 +72,16 @@
 
 namespace {
 
+#ifndef SM_PROW_WORDS
 #define SM_PROW_WORDS 128
-#define SM_QROW_WORDS 256
+#endif
+#ifndef SM_QROW_WORDS
+#define SM_QROW_WORDS 192
+#endif
 #define SM_RBUF 128
-#define FC_WORDS 448  // shared-memory copy of the warp's top frame (owner reads only)
+#ifndef FC_WORDS
+#define FC_WORDS 256  // shared-memory copy of the warp's top frame (owner reads only)
+#endif
 struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligned offset
   union {                               // never live at the same time:
     unsigned long long skey[MBE_SMEM_SORT];  //   small sorts, antichain staging / wide metadata
@@ -153,6 +162,20 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// Race-stress builds (MBE_DEBUG_DELAYS=1, scripts/stress_delays.py): a random pause of up to ~4 us at
+// one in four visits of every synchronisation point of the lock-free protocol.
+__device__ __forceinline__ void dbg_delay(uint32_t salt) {
+#if MBE_DEBUG_DELAYS
+  uint32_t r = (uint32_t)clock64() * 0x9E3779B1u ^ salt * 0x85EBCA6Bu ^ (blockIdx.x << 7) ^ threadIdx.x;
+  r ^= r >> 15;
+  r *= 0x2C1B3C6Du;
+  r ^= r >> 12;
+  if ((r & 3u) == 0u) __nanosleep((r >> 8) & 4095u);
+#else
+  (void)salt;
+#endif
 }
 
 // MBE_STATS sub-phase accounting: add the cycles since `t` to phase k and restart `t`.
@@ -897,6 +920,7 @@ __device__ __forceinline__ bool arena_reserve(Warp& w, const SearchParams& p, ui
     w.failed = true;
     return false;
   }
+  if (MBE_STATS_ON && w.lane == 0) atomicMax(&p.gl->max_arena_words, (unsigned long long)(w.atop + words));
   return true;
 }
 
@@ -919,6 +943,7 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
     w.sm->fsz[w.top] = (unsigned int)size_words;
     if (w.sm->fc_depth == (int)w.top) w.sm->fc_depth = -1;
     __threadfence();
+    dbg_delay(1);
     atomicExch(&d->claim, (((unsigned long long)nP) << 32) | first);
     p.tops[w.gw] = w.top + 1;
     if (nP - first >= 2 && !(p.flags & F_NO_STEAL)) atomicOr(&p.hint[w.gw >> 5], 1u << (w.gw & 31));
@@ -1530,7 +1555,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     bool sorted = false;
     if (!keep_all && Wc <= 4 && qn > 128) {  // descending popcount: the antichain needs no removal pass
       uint32_t* tmp = qsrc == w.pbuf ? w.qbuf : w.pbuf;
-      popc_sort_rows_desc(qsrc, qn, Wc, tmp, w.sm->sval, lane);
+      popc_sort_rows_desc(qsrc, qn, Wc, tmp, w.sm->hist, lane);  // 32 Wc + 1 <= 129 bins
       qsrc = tmp;
       sorted = true;
     }
@@ -1580,6 +1605,11 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   MBE_PHASE(10, tph);
   if (MBE_STATS_ON && lane == 0) {  // diagnostics: remember the longest list task
     const unsigned long long dt = (unsigned long long)clock64() - tstart;
+    {
+      const uint32_t b = min(11u, (31u - __clz(nt + 1u)) / 2u);
+      atomicAdd(&p.gl->list_nt_hist[0][b], 1ull);
+      atomicAdd(&p.gl->list_nt_hist[1][b], dt);
+    }
     if (atomicMax(&p.gl->longest[0], dt) < dt) {
       unsigned long long* L = p.gl->longest;
       L[1] = root ? 1ull : 0ull; L[2] = x; L[3] = dx; L[4] = nLp; L[5] = nt; L[6] = nPc; L[7] = nQc;
@@ -2082,6 +2112,7 @@ __device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const 
               const uint32_t rem = (uint32_t)(c >> 32) > (uint32_t)c ? (uint32_t)(c >> 32) - (uint32_t)c : 1u;
               k = steal_half ? max(1u, rem / 2) : 1u;
               atomicSub(&p.gl->idle, 1u);
+              dbg_delay(2);
               old = atomicAdd(cw, (unsigned long long)k);
               if ((uint32_t)old >= (uint32_t)(old >> 32)) atomicAdd(&p.gl->idle, 1u);
             }
@@ -2144,6 +2175,7 @@ __device__ __noinline__ uint32_t claim_root_shared(const SearchParams& p) {
       if (g0 < n) {
         const unsigned long long rem = n - g0;
         const unsigned long long c = (rem + p.gss_div - 1) / p.gss_div;
+        dbg_delay(3);
         pos = atomicAdd_system(p.claim_counter, c);
         if (pos < n) len = min(c, (unsigned long long)n - pos);
       }
@@ -2267,6 +2299,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       if (i >= nP) {
         // exhausted: wait for thieves still reading it, then pop
         if (lane == 0) {
+          dbg_delay(4);
           while (ld_volatile(&dsc->done) < nP - w.sm->ffirst[d]) {
             if (ld_volatile(&p.gl->error) || watchdog_expired(p, wd)) {
               set_error(p, 4u, 1ull);
@@ -2314,6 +2347,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
           const uint32_t q = claim_root_shared(p);
           pos = q == ~0u ? ~0ull : q;
         } else {
+          dbg_delay(5);
           pos = atomicAdd(&p.gl->root_cursor, 1ull) * p.world + p.rank;
         }
       }
@@ -2365,6 +2399,8 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       backoff = 64;
       registered = false;
       __threadfence();  // acquire: the victim published the frame before its claim word
+      if (lane == 0) dbg_delay(6);
+      __syncwarp();
       dsc = p.desc + (size_t)v * MBE_MAXDEPTH + vdep;
       const uint32_t off = ld_volatile(&dsc->off);
       F = reinterpret_cast<const uint32_t*>(p.ws + (size_t)v * p.ws_stride + p.o_arena) + off;
@@ -2414,6 +2450,13 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
           const uint32_t bw = 24u + (31u - __clz((F[0] >> 8) & 0xffu));
           atomicAdd(&p.gl->hist[0][bw], 1ull);
           atomicAdd(&p.gl->hist[1][bw], dt);
+          if (((F[0] >> 8) & 0xffu) >= 8u) {
+            const uint32_t bq = min(7u, (31u - __clz(F[3] + 1u)) / 2u), bp = min(7u, (31u - __clz(F[2] + 1u)) / 2u);
+            atomicAdd(&p.gl->wide_hist[0][bq], 1ull);
+            atomicAdd(&p.gl->wide_hist[1][bq], dt);
+            atomicAdd(&p.gl->wide_hist[2][bp], 1ull);
+            atomicAdd(&p.gl->wide_hist[3][bp], dt);
+          }
         }
       }
     }

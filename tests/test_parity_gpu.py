@@ -288,23 +288,23 @@ def test_shared_claim_counter_logical_ranks():
 
 def test_shared_counter_overflow_relaunch_replays_claims():
     """an arena-overflow relaunch must replay exactly the chunks this call claimed from
-    the shared counter.  A 4 KiB initial arena with MBE_ARENA_GROW overflows, relaunches, and the result
+    the shared counter.  A 256-byte initial arena with MBE_ARENA_GROW overflows, relaunches, and the result
     is still the whole (one rank) / the exact share."""
     g = I.random_bipartite(300, 260, 0.05, 3)
     want = oracle.mbea(g)
     ctr = ClaimCounter(0)
     with MBEGraph.from_graph(g) as G:
-        r = G.enumerate(claim_counter=ctr.ptr, arena_bytes=4096, flags=MBE_ARENA_GROW)
+        r = G.enumerate(claim_counter=ctr.ptr, arena_bytes=256, flags=MBE_ARENA_GROW)
         assert r.attempts > 1
         assert same(r, want)
         ctr.reset()
-        r0 = G.enumerate(rank=0, world=2, claim_counter=ctr.ptr, arena_bytes=4096, flags=MBE_ARENA_GROW)
-        r1 = G.enumerate(rank=1, world=2, claim_counter=ctr.ptr, arena_bytes=4096, flags=MBE_ARENA_GROW)
+        r0 = G.enumerate(rank=0, world=2, claim_counter=ctr.ptr, arena_bytes=256, flags=MBE_ARENA_GROW)
+        r1 = G.enumerate(rank=1, world=2, claim_counter=ctr.ptr, arena_bytes=256, flags=MBE_ARENA_GROW)
         assert r0.attempts > 1
         assert (r0.count + r1.count, (r0.hash + r1.hash) & R.MASK64) == (want.count, want.hash)
         assert r0.tasks + r1.tasks == want.tasks
         with pytest.raises(MBEError) as e:  # fixed arena: overflow is an error, never a partial count
-            G.enumerate(arena_bytes=4096)
+            G.enumerate(arena_bytes=256)
         assert e.value.code == -4
     ctr.close()
 
