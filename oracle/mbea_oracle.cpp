@@ -28,6 +28,9 @@
 //       root P is ordered by (degree, original id) = rank r(v); every P' is
 //       sorted by (|N(v)∩L'|, r(v)).  order_mode=1 pops in input order instead
 //       (result-invariant; used to check order independence on small graphs).
+//       order_mode=2 is the descending ablation: the root P
+//       by (descending degree, original id), every P' by (descending
+//       |N(v)∩L'|, r(v)), r = position in that root order.
 // One exact shortcut (result-identical): at the root, L = V, so a
 // vertex v with N(v)∩N(x) = ∅ has count 0 and Algorithm 1 ignores it (it
 // cannot break maximality since |L'| > 0 and joins neither Q' nor P').  The
@@ -68,7 +71,7 @@ struct Graph {
   std::vector<Set> adjU;             // u ∈ U → sorted N(u) ⊆ V
   std::vector<Set> adjV;             // v ∈ V → sorted N(v) ⊆ U
   std::vector<uint32_t> rank;        // r(u): position of u in ascending (deg, original id)
-  int order_mode = 0;                // 0 = ascending (|N(v)∩L|, r(v)); 1 = input order
+  int order_mode = 0;                // 0 = ascending (|N(v)∩L|, r(v)); 1 = input order; 2 = descending
   bool check = false;                // verify A = N(B), B = N(A) for every emission
   // optional listing (single-threaded use only)
   std::vector<uint32_t>* listing = nullptr;
@@ -168,12 +171,13 @@ void iteration(const Graph& g, const Set* L, const Set& R, uint32_t x, const Set
   for (uint32_t v : P) {
     uint64_t c = count_common(g.adjU[v], Lp);
     if (c == Lp.size()) Rp.push_back(v);
-    else if (c > 0) Pk.push_back({(c << 32) | g.rank[v], v});
+    else if (c > 0) Pk.push_back({((g.order_mode == 2 ? (0xffffffffULL - c) : c) << 32) | g.rank[v], v});
   }
   emit(g, Lp, Rp, acc);
   if (!Pk.empty()) {
-    // next-level order (reading Z6): ascending (|N(v) ∩ L'|, r(v)); input order keeps P's order
-    if (g.order_mode == 0) std::sort(Pk.begin(), Pk.end());
+    // next-level order (reading Z6): ascending (|N(v) ∩ L'|, r(v)); input order keeps P's order;
+    // descending (-|N(v) ∩ L'|, r(v))
+    if (g.order_mode != 1) std::sort(Pk.begin(), Pk.end());
     Set Pp;
     Pp.reserve(Pk.size());
     for (auto& kv : Pk) Pp.push_back(kv.second);
@@ -244,13 +248,23 @@ int build(Graph& g, uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uin
   return 0;
 }
 
-// Root P: degree ≥ 1 vertices, ascending (deg, id) or input (id) order.
-std::vector<uint32_t> root_order(const Graph& g) {
+// Root P: degree ≥ 1 vertices, ascending (deg, id), input (id) or descending (-deg, id) order.
+// r(v) (g.rank) is the position of v in that order, the tie-break of every later level.
+std::vector<uint32_t> root_order(Graph& g) {
+  const uint32_t nU = (uint32_t)g.adjU.size();
+  std::vector<uint32_t> all(nU);
+  for (uint32_t u = 0; u < nU; ++u) all[u] = u;
+  if (g.order_mode == 2)
+    std::sort(all.begin(), all.end(), [&](uint32_t a, uint32_t b) {
+      if (g.adjU[a].size() != g.adjU[b].size()) return g.adjU[a].size() > g.adjU[b].size();
+      return a < b;
+    });
+  else if (g.order_mode == 0)
+    std::sort(all.begin(), all.end(), [&](uint32_t a, uint32_t b) { return g.rank[a] < g.rank[b]; });
+  for (uint32_t k = 0; k < nU; ++k) g.rank[all[k]] = k;
   std::vector<uint32_t> root;
-  for (uint32_t u = 0; u < g.adjU.size(); ++u)
+  for (uint32_t u : all)
     if (!g.adjU[u].empty()) root.push_back(u);
-  if (g.order_mode == 0)
-    std::sort(root.begin(), root.end(), [&](uint32_t a, uint32_t b) { return g.rank[a] < g.rank[b]; });
   return root;
 }
 

@@ -50,6 +50,9 @@ def _load():
     return _lib
 
 
+_ORDERS = {"ascending": 0, "input": 1, "descending": 2}
+
+
 @dataclasses.dataclass
 class OracleResult:
     count: int
@@ -82,7 +85,7 @@ def mbea(g, candidate_side: int = 0, order: str = "ascending", threads: int = 0,
     lib = _load()
     rp, ci = _arrays(g)
     out = np.zeros(6, dtype=np.uint64)
-    rc = lib.oracle_mbea(g.n1, g.n2, _p64(rp), _p32(ci), candidate_side, 0 if order == "ascending" else 1,
+    rc = lib.oracle_mbea(g.n1, g.n2, _p64(rp), _p32(ci), candidate_side, _ORDERS[order],
                          threads, 1 if check else 0, _p64(out))
     if rc:
         raise ValueError(f"oracle_mbea: error {rc}")
@@ -95,7 +98,7 @@ def mbea_plain(g, candidate_side: int = 0, order: str = "ascending") -> OracleRe
     rp, ci = _arrays(g)
     out = np.zeros(6, dtype=np.uint64)
     rc = lib.oracle_mbea_plain(g.n1, g.n2, _p64(rp), _p32(ci), candidate_side,
-                               0 if order == "ascending" else 1, _p64(out))
+                               _ORDERS[order], _p64(out))
     if rc:
         raise ValueError(f"oracle_mbea_plain: error {rc}")
     return OracleResult(*[int(v) for v in out])
@@ -108,7 +111,7 @@ def mbea_roots(g, roots, candidate_side: int = 0, order: str = "ascending", thre
     roots = np.ascontiguousarray(roots, dtype=np.uint32)
     out = np.zeros((max(len(roots), 1), 4), dtype=np.uint64)
     rc = lib.oracle_mbea_roots(g.n1, g.n2, _p64(rp), _p32(ci), candidate_side,
-                               0 if order == "ascending" else 1, threads, _p32(roots), len(roots), _p64(out))
+                               _ORDERS[order], threads, _p32(roots), len(roots), _p64(out))
     if rc:
         raise ValueError(f"oracle_mbea_roots: error {rc}")
     return out[: len(roots)]
@@ -122,7 +125,7 @@ def mbea_list(g, candidate_side: int = 0, order: str = "ascending"):
     while True:
         buf = np.zeros(cap, dtype=np.uint32)
         n = lib.oracle_mbea_list(g.n1, g.n2, _p64(rp), _p32(ci), candidate_side,
-                                 0 if order == "ascending" else 1, _p32(buf), cap)
+                                 _ORDERS[order], _p32(buf), cap)
         if n < 0:
             raise ValueError(f"oracle_mbea_list: error {n}")
         if n <= cap:

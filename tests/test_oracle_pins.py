@@ -349,3 +349,24 @@ def test_tree_counters_literal_mbea_agrees_on_worked_graphs():
                     (I.crown(3), (6, 6, 0))]:
         b = oracle.mbea_plain(g)
         assert (b.count, b.tasks, b.pruned) == want, g.name
+
+
+def test_tree_order_variants_hand_derived():
+    """SURVEY §8(f) row 3 order ablations.  Descending: root P by (-deg, id), P' by (-|N(v) ∩ L'|, r(v));
+    input: root P by id, P' in its parent's order.  Derivations in the comments of the tests above:
+    nested_pair descending/input = x=0 first (child x=1), then x=1 pruned by Q=[0] -> (3, 1);
+    deep_order descending -> (7, 1) (x=2 before x=1 under x=0); deep_order input keeps [1, 2] -> (6, 0)."""
+    for g, order, want in [(nested_pair(), "descending", (2, 3, 1)), (nested_pair(), "input", (2, 3, 1)),
+                           (deep_order_graph(), "descending", (6, 7, 1)), (deep_order_graph(), "input", (6, 6, 0))]:
+        r = oracle.mbea(g, order=order)
+        assert (r.count, r.tasks, r.pruned) == want, (g.name, order)
+        b = oracle.mbea_plain(g, order=order)
+        assert (b.count, b.tasks, b.pruned) == want, (g.name, order)
+
+
+def test_descending_order_equals_bruteforce():
+    for g in _random_graphs(200, 11, 59):
+        truth = R.maximal_bicliques_closure(g)
+        for side in (1, 2):
+            r = oracle.mbea(g, candidate_side=side, order="descending")
+            assert (r.count, r.hash) == (len(truth), R.result_hash(truth))
