@@ -96,7 +96,16 @@ typedef struct {
   uint32_t defer_min;        /* wide (8/16-word) list-path children with |P'| * |Q'| >= defer_min publish every
                                 task with Step 3 deferred to the task (result-invariant); 0 = auto (65536),
                                 0xffffffff = never */
+  uint32_t order;            /* candidate order (the order ablation; count and hash are
+                                order-invariant, the search tree is not): MBE_ORDER_ASCENDING (0, default: the
+                                paper's iMBE order: root P by (degree, id), every P' by
+                                (|N(v) ∩ L'|, r(v))), MBE_ORDER_INPUT (1: root P by original id, every P' in its
+                                parent's order), MBE_ORDER_DESCENDING (2: root P by (-degree, id), every P' by
+                                (-|N(v) ∩ L'|, r(v))); r(v) = position in the root order.  Else MBE_EINVAL. */
 } mbe_config;
+#define MBE_ORDER_ASCENDING 0u
+#define MBE_ORDER_INPUT 1u
+#define MBE_ORDER_DESCENDING 2u
 
 /* Optional bounded listing; caller-owned HOST buffers.  Record r occupies
  * ids[rec_off[r] .. rec_off[r] + rec_n1[r] + rec_n2[r]): first the side-1 ids

@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("MBE_LIB_PATH") or os.path.join(_HERE, "libmbe.so")
 MBE_OK, MBE_EINVAL, MBE_ENOMEM, MBE_ECUDA, MBE_EOVERFLOW, MBE_ERANGE, MBE_EDIST, MBE_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7
 MBE_NO_STEAL, MBE_STATS, MBE_NO_ANTICHAIN, MBE_NO_TWIN, MBE_STEAL_ONE, MBE_STEAL_HALF = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 MBE_ARENA_GROW = 0x40
+MBE_ORDER = {"ascending": 0, "input": 1, "descending": 2}
 
 EXPORTED_SYMBOLS = ("mbe_load_csr", "mbe_enumerate", "mbe_get_info", "mbe_free", "mbe_release_workspaces",
                     "mbe_strerror", "mbe_last_error_detail", "mbe_format_listing", "mbe_counter_create",
@@ -36,7 +37,7 @@ class mbe_config(ctypes.Structure):
     _fields_ = [("struct_size", _u32), ("ctas_per_sm", _u32), ("threads_per_cta", _u32),
                 ("bitmap_threshold", _u32), ("candidate_side", _i32), ("flags", _u32), ("rank", _u32),
                 ("world", _u32), ("claim_counter", _vp), ("arena_bytes", _u64), ("stream", _vp),
-                ("per_root", _p64), ("watchdog_ms", _u32), ("defer_min", _u32)]
+                ("per_root", _p64), ("watchdog_ms", _u32), ("defer_min", _u32), ("order", _u32)]
 
 
 class mbe_output(ctypes.Structure):
@@ -176,7 +177,7 @@ def mbe_load_csr(n1: int, n2: int, row_ptr, col_idx, device: int = 0, flags: int
 
 def make_config(ctas_per_sm: int = 0, threads_per_cta: int = 0, bitmap_threshold: int = 0, candidate_side: int = 0,
                 flags: int = 0, rank: int = 0, world: int = 1, claim_counter: int = 0, arena_bytes: int = 0,
-                stream: int = 0, per_root=None, watchdog_ms: int = 0, defer_min: int = 0) -> mbe_config:
+                stream: int = 0, per_root=None, watchdog_ms: int = 0, defer_min: int = 0, order=0) -> mbe_config:
     c = mbe_config()
     c.struct_size = ctypes.sizeof(mbe_config)
     c.ctas_per_sm = ctas_per_sm
@@ -192,6 +193,7 @@ def make_config(ctas_per_sm: int = 0, threads_per_cta: int = 0, bitmap_threshold
     c.per_root = per_root.ctypes.data_as(_p64) if per_root is not None else None
     c.watchdog_ms = watchdog_ms
     c.defer_min = defer_min
+    c.order = MBE_ORDER[order] if isinstance(order, str) else int(order)
     return c
 
 

@@ -257,7 +257,7 @@ struct mbe_graph {
   uint64_t nE = 0;
   // deduplicated host CSR in both directions (original ids)
   std::vector<uint32_t> off1, adj1, off2, adj2;
-  Side side[2];
+  Side side[2][3];  // [candidate side - 1][candidate order]
   uint64_t h2d_bytes = 0;  // bytes uploaded by ingest (all built sides)
   SearchParams sp;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -266,7 +266,8 @@ struct mbe_graph {
   DevBuf claim_tab;             // shared-counter claim log of the current call ([n_roots + 1] u64)
   ~mbe_graph() {
     claim_tab.release();
-    for (auto& s : side) s.release();
+    for (auto& so : side)
+      for (auto& s : so) s.release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
   }
@@ -275,8 +276,8 @@ struct mbe_graph {
 namespace {
 
 // Build the device graph for candidate side s (1 = rows, 2 = cols).
-int build_side(mbe_graph* g, int s) {
-  Side& S = g->side[s - 1];
+int build_side(mbe_graph* g, int s, uint32_t order = 0) {
+  Side& S = g->side[s - 1][order];
   if (S.built) return MBE_OK;
   g_upload_counter = &g->h2d_bytes;
   const bool dbg = std::getenv("MBE_DEBUG_TIMING") != nullptr;
@@ -292,16 +293,21 @@ int build_side(mbe_graph* g, int s) {
   const uint32_t nU = s == 1 ? g->n1 : g->n2, nV = s == 1 ? g->n2 : g->n1;
   S.nU = nU;
   S.nV = nV;
-  // rank by ascending (degree, original id): counting sort over degrees (stable in id)
+  // rank = position in the root order: ascending (degree, original id) by a counting sort over degrees
+  // (stable in id); descending (-degree, id) by the same sort over maxdeg - degree; input = original id
   uint32_t maxdeg = 0;
   for (uint32_t u = 0; u < nU; ++u) maxdeg = std::max(maxdeg, offC[u + 1] - offC[u]);
+  auto dkey = [&](uint32_t u) {
+    const uint32_t d = offC[u + 1] - offC[u];
+    return order == 2 ? maxdeg - d : (order == 1 ? 0u : d);
+  };
   std::vector<uint32_t> bucket(maxdeg + 2, 0);
-  for (uint32_t u = 0; u < nU; ++u) bucket[offC[u + 1] - offC[u] + 1]++;
+  for (uint32_t u = 0; u < nU; ++u) bucket[dkey(u) + 1]++;
   for (uint32_t d = 1; d < bucket.size(); ++d) bucket[d] += bucket[d - 1];
   S.origU.assign(nU, 0);
   S.rankU.assign(nU, 0);
   for (uint32_t u = 0; u < nU; ++u) {
-    uint32_t r = bucket[offC[u + 1] - offC[u]]++;
+    uint32_t r = bucket[dkey(u)]++;
     S.origU[r] = u;
     S.rankU[u] = r;
   }
@@ -379,9 +385,9 @@ int build_side(mbe_graph* g, int s) {
     }
   }
   lap("root cost + sort");
-  std::vector<uint32_t> order(key.size());
-  for (size_t k = 0; k < key.size(); ++k) order[k] = (uint32_t)key[k];
-  S.n_roots = (uint32_t)order.size();
+  std::vector<uint32_t> exec(key.size());  // execution order of the level-1 subtrees
+  for (size_t k = 0; k < key.size(); ++k) exec[k] = (uint32_t)key[k];
+  S.n_roots = (uint32_t)exec.size();
   Packer pk;
   pk.add(S.offU, offU.data(), offU.size() * 4);
   pk.add(S.adjU, adjU.data(), adjU.size() * 4);
@@ -390,7 +396,7 @@ int build_side(mbe_graph* g, int s) {
   pk.add(S.hvU, hvU.data(), hvU.size() * 8);
   pk.add(S.hvV, hvV.data(), hvV.size() * 8);
   pk.add(S.origUd, S.origU.data(), S.origU.size() * 4);
-  pk.add(S.root_order, order.data(), order.size() * 4);
+  pk.add(S.root_order, exec.data(), exec.size() * 4);
   pk.add(S.twin, nullptr, nU);  // written by the twin pre-pass
   int rc = pk.commit(S.all, g_upload_counter);
   if (rc) {
@@ -684,15 +690,16 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     return fail(MBE_EINVAL, "threads_per_cta must be a multiple of 32 <= " + std::to_string(MBE_BLOCK));
   if (cfg.bitmap_threshold > 32 * MBE_WMAX) return fail(MBE_EINVAL, "bitmap_threshold > 512");
   if (cfg.candidate_side < 0 || cfg.candidate_side > 2) return fail(MBE_EINVAL, "candidate_side");
+  if (cfg.order > 2) return fail(MBE_EINVAL, "order must be MBE_ORDER_ASCENDING, _INPUT or _DESCENDING");
   if (out && (out->cap_records && (!out->rec_off || !out->rec_n1 || !out->rec_n2)))
     return fail(MBE_EINVAL, "mbe_output buffers");
   if (out && out->cap_ids && !out->ids) return fail(MBE_EINVAL, "mbe_output.ids");
   std::memset(res, 0, sizeof(*res));
   CUDA_TRY(cudaSetDevice(g->device));
   const int side = cfg.candidate_side ? cfg.candidate_side : (g->n2 < g->n1 ? 2 : 1);
-  int rc = build_side(g, side);
+  int rc = build_side(g, side, cfg.order);
   if (rc) return rc;
-  Side& S = g->side[side - 1];
+  Side& S = g->side[side - 1][cfg.order];
   res->candidate_side = side;
   if (S.nU == 0 || g->nE == 0 || S.n_roots == 0) {
     res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -752,7 +759,9 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
                        (const uint32_t*)S.offV.p, (const uint32_t*)S.adjV.p, (const uint64_t*)S.hvU.p,
                        (const uint64_t*)S.hvV.p, (const uint32_t*)S.origUd.p, (const uint32_t*)S.root_order.p,
                        (const uint8_t*)S.twin.p, S.n_roots, S.maxdegU};
-  if (!(cfg.flags & MBE_NO_TWIN) && !S.twin_ready) {
+  // (twin pruning relies on ascending degrees; the order ablations run without it)
+  const bool twin = !(cfg.flags & MBE_NO_TWIN) && cfg.order == 0;
+  if (twin && !S.twin_ready) {
     if (mbe_launch_twin(dg, g->sm_count, st) != 0)
       return fail(MBE_ECUDA, std::string("twin kernel launch: ") + cudaGetErrorString(cudaGetLastError()));
     S.twin_ready = true;
@@ -836,7 +845,8 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.dedup_min = MBE_DEDUP_MIN;
     p.defer_min = cfg.defer_min == 0 ? MBE_DEFER_MIN_DEFAULT : (cfg.defer_min == 0xffffffffu ? 0u : cfg.defer_min);
     p.wide_acmax = MBE_WIDE_ACMAX;
-    p.flags = cfg.flags;
+    p.flags = cfg.flags | (twin ? 0u : (uint32_t)MBE_NO_TWIN);
+    p.order = cfg.order;
     p.rank = cfg.rank;
     p.world = cfg.world;
     p.claim_counter = reinterpret_cast<unsigned long long*>(cfg.claim_counter);

@@ -112,6 +112,7 @@ struct SearchParams {
   uint32_t wide_acmax;  // wide (8/16-word) list-path children keep more distinct Q' rows than this unreduced
   uint32_t ac_min, ac_ratio;  // list-path children skip the antichain if |Q'| > ac_min and > ac_ratio*(|P'|+1)   // list-path children with more Q' candidates are deduplicated before the antichain
   uint32_t flags;
+  uint32_t order;  // 0 ascending (default), 1 input, 2 descending (mbe_config.order)
   uint32_t rank, world;
   unsigned long long* claim_counter;  // NULL -> static deal; else shared across ranks (system-scope atomics)
   unsigned long long* claim_tab;      // [n_roots + 1] chunks claimed by this call: (local base << 32) | global start

@@ -411,6 +411,20 @@ __device__ __noinline__ void sort_radix(unsigned long long* key, uint32_t* val, 
 
 __device__ __forceinline__ uint32_t bit_length(uint32_t x) { return x ? 32u - __clz(x) : 0u; }
 
+// Sort keys of child candidates (mbe_config.order): ascending (c, r) is the paper's iMBE order
+// (P:491-493); the input (r) and descending (-c, r) orders are the ablation.
+// c = |N(v) ∩ L'| < maxc, v = r(v) (internal id = position in the root order).
+__device__ __forceinline__ unsigned long long order_key(uint32_t order, uint32_t c, uint32_t v, uint32_t maxc) {
+  if (order == 1u) return ((unsigned long long)v << 32) | c;
+  return ((unsigned long long)(order == 2u ? maxc - c : c) << 32) | v;
+}
+__device__ __forceinline__ uint32_t key_id(uint32_t order, unsigned long long k) {
+  return order == 1u ? (uint32_t)(k >> 32) : (uint32_t)k;
+}
+__device__ __forceinline__ uint32_t key_count(uint32_t order, unsigned long long k, uint32_t maxc) {
+  return order == 1u ? (uint32_t)k : (order == 2u ? maxc - (uint32_t)(k >> 32) : (uint32_t)(k >> 32));
+}
+
 __device__ __noinline__ void sort_pairs_small(unsigned long long* key, uint32_t* val, uint32_t n, WarpSmem* sm, int lane) {
   if (n <= 1) return;
   if (n <= 32) sort_regs32(key, val, n, lane);
@@ -427,7 +441,9 @@ __device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint
     // second buffers live right after the first ones (same per-warp region, sized nU)
     unsigned long long* key2 = w.skey + p.skey2_off;
     uint32_t* val2 = w.sval + p.skey2_off;
-    sort_radix(w.skey, w.sval, key2, val2, n, bit_length(p.g.nU), bit_length(max_count), w.sm, w.lane);
+    const uint32_t ib = bit_length(p.g.nU), cb = bit_length(max_count);
+    if (p.order == 1u) sort_radix(w.skey, w.sval, key2, val2, n, cb, ib, w.sm, w.lane);
+    else sort_radix(w.skey, w.sval, key2, val2, n, ib, cb, w.sm, w.lane);
   }
 }
 
@@ -1063,7 +1079,7 @@ __device__ __forceinline__ bool prune_q_rows(const Row<W>& r, bool alive, const 
 // Row t (ascending key order) is Pr[perm[t]] (perm == nullptr: Pr[t]).
 template <int W>
 __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t* perm, uint32_t nP, const uint32_t* Qr,
-                                             uint32_t nQ, uint32_t* S, int lane) {
+                                             uint32_t nQ, uint32_t* S, int lane, bool ascending = true) {
   uint32_t nS = 0;
   for (uint32_t tb = 0; tb < nP; tb += 32) {
     const uint32_t t = tb + lane;
@@ -1074,6 +1090,10 @@ __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t*
     for (int q = 0; q < W; ++q) key += __popc(r.w[q]);
     for (int j = (int)t - 1; alive && j >= 0; --j) {
       const Row<W> s = load_row<W>(Pr + (size_t)(perm ? perm[j] : (uint32_t)j) * W);
+      if (!ascending) {  // order ablation: any earlier sibling may contain row t
+        if (row_subset<W>(r, s)) alive = false;
+        continue;
+      }
       uint32_t kj = 0;
 #pragma unroll
       for (int q = 0; q < W; ++q) kj += __popc(s.w[q]);
@@ -1097,7 +1117,8 @@ __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t*
 #endif
 __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t nP, const uint32_t* Qr, uint32_t nQ,
                                                   uint32_t W, uint32_t* S, unsigned long long* meta,
-                                                  uint32_t* cmask_buf, int lane, unsigned long long* prof = nullptr) {
+                                                  uint32_t* cmask_buf, int lane, unsigned long long* prof = nullptr,
+                                                  bool ascending = true) {
   unsigned long long c0 = prof ? (unsigned long long)clock64() : 0ull, ca = 0, cb = 0;
   for (uint32_t t = lane; t < nP + nQ; t += 32)
     meta[t] = wide_meta(t < nP ? Pr + (size_t)t * W : Qr + (size_t)(t - nP) * W, W);
@@ -1137,6 +1158,10 @@ __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t n
     const uint32_t key = (uint32_t)(mr >> MBE_META_SHIFT);
     for (int j = (int)t - 1; alive && j >= 0; --j) {
       const unsigned long long mj = meta[j];
+      if (!ascending) {  // order ablation: any earlier sibling may contain row t
+        if (meta_may_subset(mr, mj) && wide_subset(r, Pr + (size_t)j * W, W)) alive = false;
+        continue;
+      }
       if ((uint32_t)(mj >> MBE_META_SHIFT) != key) break;
       if (mj == mr && wide_eq(r, Pr + (size_t)j * W, W)) alive = false;
     }
@@ -1201,12 +1226,13 @@ __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t n
 
 __device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr, uint32_t nP, const uint32_t* Qr,
                                                   uint32_t nQ, uint32_t* S, unsigned long long* meta,
-                                                  uint32_t* cmask_buf, int lane, unsigned long long* prof = nullptr) {
+                                                  uint32_t* cmask_buf, int lane, unsigned long long* prof = nullptr,
+                                                  bool ascending = true) {
   __syncwarp();
-  if (W == 1) return prune_frame<1>(Pr, nullptr, nP, Qr, nQ, S, lane);
-  if (W == 2) return prune_frame<2>(Pr, nullptr, nP, Qr, nQ, S, lane);
-  if (W == 4) return prune_frame<4>(Pr, nullptr, nP, Qr, nQ, S, lane);
-  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, meta, cmask_buf, lane, prof);
+  if (W == 1) return prune_frame<1>(Pr, nullptr, nP, Qr, nQ, S, lane, ascending);
+  if (W == 2) return prune_frame<2>(Pr, nullptr, nP, Qr, nQ, S, lane, ascending);
+  if (W == 4) return prune_frame<4>(Pr, nullptr, nP, Qr, nQ, S, lane, ascending);
+  return prune_frame_wide(Pr, nP, Qr, nQ, W, S, meta, cmask_buf, lane, prof, ascending);
 }
 
 // Account the nP tasks of a child frame decided at build time (nS survive the check).  Algorithmic
@@ -1452,7 +1478,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     }
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
-      w.skey[idx] = ((unsigned long long)c << 32) | v;
+      w.skey[idx] = order_key(p.order, c, v, nLp);
       w.sval[idx] = idx;
       if (bm) {
         for (uint32_t q = 0; q < Wc && q < 4; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
@@ -1517,7 +1543,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   uint32_t* CP = CR + nRp;
   for (uint32_t t = lane; t < nLp; t += 32) CL[t] = Lp[t];
   for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
-  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, w.skey[t]);
   uint64_t size;
   uint32_t nQk = 0;
   uint32_t nT = nPc;  // tasks published (bit-row children: the survivors of the eager check)
@@ -1575,7 +1601,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       for (uint32_t t = lane; t < nPc; t += 32) S[t] = t;
       nT = nPc;
     } else {
-      nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, w.pbuf, lane, MBE_STATS_ON ? pprof : nullptr);
+      nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, w.pbuf, lane, MBE_STATS_ON ? pprof : nullptr, p.order == 0u);
       account_children(w, p, nPc, nT, Wc, nQk);
     }
     if MBE_STATS_ON {
@@ -1585,7 +1611,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     size = (uint64_t)(S + nT - C);
   } else {
     uint32_t* CK = CP + nPc;
-    for (uint32_t t = lane; t < nPc; t += 32) CK[t] = (uint32_t)(w.skey[t] >> 32);
+    for (uint32_t t = lane; t < nPc; t += 32) CK[t] = key_count(p.order, w.skey[t], nLp);
     size = (uint64_t)(CK + nPc - C);
   }
   if (nT > 0) {
@@ -1674,7 +1700,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
-      kbuf[idx] = ((unsigned long long)c << 32) | v;
+      kbuf[idx] = order_key(p.order, c, v, k);
       vbuf[idx] = idx;
       uint32_t out[4];
       mbe_compress_apply_w<W>(cmp, r.w, out);
@@ -1732,7 +1758,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   if (nPc == 1) {
     // The child frame would hold ONE task: x2 = P'[0] with L'' = row'(x2), Q-role = Q', P-role = ∅
     // (Algorithm 1 on a one-element P).  Run it inline instead of building/publishing a frame.
-    const uint32_t x2 = (uint32_t)kbuf[0];
+    const uint32_t x2 = key_id(p.order, kbuf[0]);
     uint32_t r2[4] = {0u, 0u, 0u, 0u};
     for (uint32_t q = 0; q < Wn; ++q) r2[q] = pbuf[q];
     bool dom = false;
@@ -1785,9 +1811,10 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   // their antichain does), before anything is written: most children end here with no survivor.
   uint32_t* Stmp = w.touched;
   __syncwarp();
-  const uint32_t nS = Wn == 1   ? prune_frame<1>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
-                      : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane)
-                                : prune_frame<4>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane);
+  const bool asc = p.order == 0u;
+  const uint32_t nS = Wn == 1   ? prune_frame<1>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane, asc)
+                      : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane, asc)
+                                : prune_frame<4>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane, asc);
   MBE_PHASE(15, tph);
   if (nS == 0) {
     account_children(w, p, nPc, 0, Wn, MBE_STATS_ON ? stats_r1_size(Wn, qbuf, nQc, w, p) : 0u);
@@ -1803,7 +1830,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   uint32_t* CP = CR + nRp;
   for (uint32_t t = lane; t < k; t += 32) CL[t] = lbuf[t];
   for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : rbuf[t - nR - 1]);
-  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)kbuf[t];
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, kbuf[t]);
   uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
   for (uint32_t t = lane; t < nPc; t += 32) {
     uint32_t src = vbuf[t];
@@ -1907,7 +1934,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     const uint32_t bp = __ballot_sync(FULLMASK, isPc);
     if (isPc) {
       const uint32_t idx = nPc + __popc(bp & lanemask_lt());
-      w.skey[idx] = ((unsigned long long)c << 32) | v;
+      w.skey[idx] = order_key(p.order, c, v, k);
       w.sval[idx] = idx;
       w.pbuf[idx] = j;
     }
@@ -1976,7 +2003,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   uint32_t* CP = CR + nRp;
   for (uint32_t t = lane; t < k; t += 32) CL[t] = w.lbuf[t];
   for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
-  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = (uint32_t)w.skey[t];
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, w.skey[t]);
   uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
   uint32_t* cm = reinterpret_cast<uint32_t*>(w.sm->posv);  // compression masks (posv is free here)
   compress_prep_lanes(lx, W, cm, lane);
@@ -1992,7 +2019,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   uint32_t* Stmp = w.touched;
   MBE_PHASE(14, tph);
   wide_sub(29);
-  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, w.pbuf, lane);
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, w.pbuf, lane, nullptr, p.order == 0u);
   MBE_PHASE(15, tph);
   wide_sub(30);
   if (nS == 0) {

@@ -393,3 +393,25 @@ def test_full_config_sampled_roots_vs_oracle(cfg):
     assert np.array_equal(pr[sample], want)
     assert int(pr[:, 0].sum()) == r.count
     assert int(pr[:, 2].sum()) == r.tasks
+
+
+# ------------------------------------------------------------------ candidate-order ablation
+@pytest.mark.parametrize("order", ["input", "descending"])
+def test_order_variants_match_oracle_tree(order):
+    """mbe_config.order: the GPU builds the oracle's search tree under the same order (tasks, pruned equal),
+    and the result is order-invariant (count, hash equal the ascending run)."""
+    from test_oracle_pins import deep_order_graph, nested_pair, tie_break_graph
+
+    graphs = [nested_pair(), deep_order_graph(), tie_break_graph(), I.crown(8), I.erdos_renyi_c1b(),
+              I.random_bipartite(30, 500, 0.5, 6), I.random_bipartite(12, 400, 0.7, 1)]
+    graphs += list(_random_graphs(60, 40, 313))
+    for g in graphs:
+        want = oracle.mbea(g, order=order)
+        asc = oracle.mbea(g)
+        for cfg in (dict(), dict(flags=MBE_STEAL_HALF), dict(defer_min=1), dict(bitmap_threshold=64)):
+            r = gpu(g, order=order, **cfg)
+            assert same(r, want), (g.name, order, cfg)
+        assert (want.count, want.hash) == (asc.count, asc.hash)
+    for side in (1, 2):  # both candidate sides
+        g = I.erdos_renyi_c1b(120, 90)
+        assert same(gpu(g, order=order, candidate_side=side), oracle.mbea(g, order=order, candidate_side=side))
