@@ -66,6 +66,9 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t *row_ptr, const uint32
 #define MBE_NO_TWIN 0x8u      /* disable root-level twin pre-pruning (result-invariant) */
 #define MBE_STEAL_ONE 0x10u   /* thieves take one task at a time (the default since round 1; kept for compatibility) */
 #define MBE_STEAL_HALF 0x20u  /* thieves take half of a frame's unclaimed tasks and copy the frame (result-invariant; slower on C2-C5) */
+#define MBE_NO_RS 0x80u       /* ablation: counts |N(v) ∩ L'| of list-path tasks by forward intersection instead
+                                 of reverse scanning (the paper's noRS; result- and tree-invariant;
+                                 runs the instrumented kernel) */
 #define MBE_ARENA_GROW 0x40u  /* arena_bytes is the INITIAL per-warp arena: grow it x4 and relaunch on overflow
                                  (always the case when arena_bytes = 0) */
 

@@ -10,6 +10,7 @@ missing (no CPU fallback).
 from ._lib import (  # noqa: F401
     EXPORTED_SYMBOLS,
     MBE_ARENA_GROW,
+    MBE_NO_RS,
     ClaimCounter,
     MBE_NO_ANTICHAIN,
     MBE_NO_STEAL,

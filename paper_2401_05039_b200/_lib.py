@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("MBE_LIB_PATH") or os.path.join(_HERE, "libmbe.so")
 MBE_OK, MBE_EINVAL, MBE_ENOMEM, MBE_ECUDA, MBE_EOVERFLOW, MBE_ERANGE, MBE_EDIST, MBE_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7
 MBE_NO_STEAL, MBE_STATS, MBE_NO_ANTICHAIN, MBE_NO_TWIN, MBE_STEAL_ONE, MBE_STEAL_HALF = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 MBE_ARENA_GROW = 0x40
+MBE_NO_RS = 0x80
 MBE_ORDER = {"ascending": 0, "input": 1, "descending": 2}
 
 EXPORTED_SYMBOLS = ("mbe_load_csr", "mbe_enumerate", "mbe_get_info", "mbe_free", "mbe_release_workspaces",

@@ -709,7 +709,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
   const uint32_t threads = cfg.threads_per_cta ? cfg.threads_per_cta : MBE_BLOCK;
   // persistent kernel: every CTA must be co-resident, so clamp to the occupancy limit (cached per handle)
   // instrumented kernel instantiation only when stats / per-root counters / a listing are requested
-  const bool instr = (cfg.flags & MBE_STATS) || cfg.per_root || (out && out->cap_records);
+  const bool instr = (cfg.flags & (MBE_STATS | MBE_NO_RS)) || cfg.per_root || (out && out->cap_records);
   const int smem_warp = instr ? mbe_search_smem_per_warp_instr() : mbe_search_smem_per_warp();
   int& occ = g->occ[instr ? 1 : 0][threads / 32 - 1];
   if (occ <= 0)

@@ -146,6 +146,7 @@ struct SearchParams {
 #define F_NO_TWIN 0x8u
 #define F_STEAL_ONE 0x10u
 #define F_STEAL_HALF 0x20u
+#define F_NO_RS 0x80u
 
 // Launches the twin pre-pass and the persistent search kernel on `stream`;
 // ev0/ev1 (cudaEvent_t) bracket the search kernel alone.

@@ -59,6 +59,9 @@
 #ifndef MBE_COMPRESS_ROWS
 #define MBE_COMPRESS_ROWS 1  // wide column compression: rows per lane in flight (1 with a 2-way word unroll was best; 2 and 4 slower)
 #endif
+#ifndef MBE_EXW_UNROLL
+#define MBE_EXW_UNROLL 0  // 1: copy the staged extension words with compile-time indices
+#endif
 #ifndef MBE_CLS_MLP
 #define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification (2 -> 4: C5 80 -> 68 ms)
 #endif
@@ -81,6 +84,14 @@ namespace {
 #define SM_RBUF 128
 #ifndef FC_WORDS
 #define FC_WORDS 256  // shared-memory copy of the warp's top frame (owner reads only)
+#endif
+#ifndef MBE_ACC_SMEM
+#define MBE_ACC_SMEM 0  // 1: lane-0 result accumulators in shared memory instead of registers
+#endif
+#if MBE_ACC_SMEM
+#define WACC(f) (w.sm->a_##f)
+#else
+#define WACC(f) (w.f)
 #endif
 struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligned offset
   union {                               // never live at the same time:
@@ -110,6 +121,12 @@ struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligne
   };
   unsigned int lbuf[128];            // L' ids
   unsigned int rbuf[SM_RBUF];        // expanded R' vertices
+#if MBE_ACC_SMEM
+  // lane-0 result accumulators (in shared memory instead of registers; measured slower, off)
+  unsigned long long a_count, a_hash, a_tasks, a_pruned, a_steals, a_list_tasks, a_bitmap_tasks, a_frames;
+  unsigned long long a_ab_list, a_ab_bit, a_ab_write;
+  unsigned int a_max_depth, a_pad;
+#endif
 };
 #define PEND_NONE 0xffffffffu
 #define SM_KEPT_WORDS (MBE_SMEM_SORT * 2)  // antichain kept list staged in skey's storage
@@ -135,10 +152,12 @@ struct Warp {
   WarpSmem* sm;
   uint32_t cur_root;
   bool failed;
+#if !MBE_ACC_SMEM
   // lane-0 accumulators
   unsigned long long count, hash, tasks, pruned, steals, list_tasks, bitmap_tasks, frames;
   unsigned long long ab_list, ab_bit, ab_write;  // MBE_STATS algorithmic bytes: list tasks, bit-row tasks, frame writes
   uint32_t max_depth;
+#endif
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -594,6 +613,17 @@ __device__ __noinline__ uint32_t dedup_hash_rows(const uint32_t* src, uint32_t n
       }
       h = h * 0x85EBCA6Bu;
       h ^= h >> 13;
+      // lanes of this step holding the same row: only the lowest one probes the table (equal rows
+      // in one warp step would otherwise serialise their CAS on one entry)
+      const uint32_t peers = __match_any_sync(__activemask(), h);
+      const int lead = __ffs(peers) - 1;
+      if (lead != lane) {
+        const uint32_t* o = src + (size_t)(base + lead) * W;
+        bool eq = true;
+        for (uint32_t q = 0; q < W && eq; ++q) eq = o[q] == r[q];
+        if (eq) goto decided;  // duplicate of the leader's row (the leader keeps or drops it)
+      }
+      {
       const unsigned long long mine = ((unsigned long long)h << 32) | (t + 1);
       uint32_t slot = h & mask;
       for (;;) {
@@ -610,6 +640,8 @@ __device__ __noinline__ uint32_t dedup_hash_rows(const uint32_t* src, uint32_t n
         }
         slot = (slot + 1) & mask;
       }
+      }
+    decided:;
     }
     const uint32_t bk = __ballot_sync(FULLMASK, keep);
     if (keep) {
@@ -872,8 +904,8 @@ __device__ __forceinline__ uint64_t align4(uint64_t x) { return (x + 3) & ~3ull;
 // Per-task accounting (tasks/pruned), lane 0.
 __device__ __forceinline__ void account_task(Warp& w, const SearchParams& p, bool pruned) {
   if (w.lane == 0) {
-    w.tasks++;
-    if (pruned) w.pruned++;
+    WACC(tasks)++;
+    if (pruned) WACC(pruned)++;
     if (MBE_PER_ROOT) {
       atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 2], 1ull);
       if (pruned) atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 3], 1ull);
@@ -885,8 +917,8 @@ __device__ __forceinline__ void account_emit(Warp& w, const SearchParams& p, uin
                                              uint32_t nR) {
   if (w.lane == 0) {
     uint64_t h = mbe_biclique_hash(p.cand_side, sL, nL, sR, nR);
-    w.count++;
-    w.hash += h;
+    WACC(count)++;
+    WACC(hash) += h;
     if (MBE_PER_ROOT) {
       atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 0], 1ull);
       atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 1], (unsigned long long)h);
@@ -963,11 +995,11 @@ __device__ void publish_frame(Warp& w, const SearchParams& p, uint64_t size_word
     atomicExch(&d->claim, (((unsigned long long)nP) << 32) | first);
     p.tops[w.gw] = w.top + 1;
     if (nP - first >= 2 && !(p.flags & F_NO_STEAL)) atomicOr(&p.hint[w.gw >> 5], 1u << (w.gw & 31));
-    w.frames++;
+    WACC(frames)++;
   }
   w.atop = align4(w.atop + size_words);
   w.top += 1;
-  if (w.lane == 0 && w.top > w.max_depth) w.max_depth = w.top;
+  if (w.lane == 0 && w.top > WACC(max_depth)) WACC(max_depth) = w.top;
   __syncwarp();
 }
 
@@ -998,6 +1030,7 @@ __device__ __noinline__ void compress_rows_lanes(const uint32_t* F, const uint32
 #pragma unroll 2
     for (uint32_t q = 0; q < W; ++q) {
       const uint32_t m = lx[q];
+      if (m == 0u) continue;  // a zero word of row(x) contributes no column (and no load)
       uint32_t y[MBE_COMPRESS_ROWS];
 #pragma unroll
       for (int k = 0; k < MBE_COMPRESS_ROWS; ++k) y[k] = ok[k] ? src[k][q] & m : 0u;
@@ -1241,15 +1274,15 @@ __device__ __forceinline__ uint32_t prune_frame_w(uint32_t W, const uint32_t* Pr
 __device__ __forceinline__ void account_children(Warp& w, const SearchParams& p, uint32_t nP, uint32_t nS,
                                                  uint32_t W, uint32_t nQ) {
   if (w.lane == 0) {
-    w.tasks += nP;
-    w.pruned += nP - nS;
+    WACC(tasks) += nP;
+    WACC(pruned) += nP - nS;
     if (MBE_PER_ROOT) {
       atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 2], (unsigned long long)nP);
       atomicAdd(&MBE_PER_ROOT[(size_t)w.cur_root * 4 + 3], (unsigned long long)(nP - nS));
     }
     if (MBE_STATS_ON) {
-      w.bitmap_tasks += nP;
-      w.ab_bit += (unsigned long long)nP * 4ull * W * (1ull + nP + nQ);
+      WACC(bitmap_tasks) += nP;
+      WACC(ab_bit) += (unsigned long long)nP * 4ull * W * (1ull + nP + nQ);
     }
   }
 }
@@ -1291,7 +1324,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   // twin pre-pruning at the root (R2 at level 1: an earlier vertex with N(v) = N(x))
   if (root && !(p.flags & F_NO_TWIN) && g.twin[x]) {
     account_task(w, p, true);
-    if (lane == 0 && MBE_STATS_ON) w.list_tasks++;
+    if (lane == 0 && MBE_STATS_ON) WACC(list_tasks)++;
     return;
   }
 
@@ -1373,9 +1406,17 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
         vv[j] = fv[j] ? __ldg(&g.adjV[o_st + (f - (o_incl - o_d))]) : 0u;
       }
       uint32_t old[MBE_SCAN_MLP];
+#if MBE_INSTR
+      if (p.flags & F_NO_RS) {  // noRS ablation: the scan only discovers the vertices (counts below)
+#pragma unroll
+        for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicExch(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
+      } else
+#endif
+      {
 #pragma unroll
       for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
-      if (bm) {
+      }
+      if (bm && !(MBE_INSTR && (p.flags & F_NO_RS))) {
 #pragma unroll
         for (int j = 0; j < MBE_SCAN_MLP; ++j)
           if (fv[j]) {
@@ -1396,6 +1437,42 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   }
   sL = warp_sum64(sL);
   __syncwarp();
+#if MBE_INSTR
+  if (p.flags & F_NO_RS) {
+    // noRS ablation (the paper's "without reverse scanning"): every discovered vertex v
+    // gets c = |N(v) ∩ L'| by forward intersection, each element of N(v) binary-searched in the
+    // sorted L' (P:138-161 as written), and its bit row from the positions found
+    unsigned long long fwd = 0;
+    for (uint32_t t = lane; t < nt; t += 32) {
+      const uint32_t v = w.touched[t];
+      const uint32_t* Nv = g.adjU + g.offU[v];
+      const uint32_t dv = g.offU[v + 1] - g.offU[v];
+      uint32_t c = 0;
+      for (uint32_t e = 0; e < dv; ++e) {
+        uint32_t lo = 0, hi = nLp;
+        const uint32_t y = Nv[e];
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (Lp[mid] < y) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < nLp && Lp[lo] == y) {
+          ++c;
+          if (bm) {
+            const uint32_t q = lo >> 5;
+            uint32_t* wd = q < 4 ? &w.slot[(size_t)v * MBE_SLOT_WORDS + 4 + q] : &w.sext[(size_t)v * MBE_SEXT_WORDS + q - 4];
+            *wd |= 1u << (lo & 31);
+          }
+        }
+      }
+      w.slot[(size_t)v * MBE_SLOT_WORDS] = c;
+      fwd += dv;
+    }
+    fwd = warp_sum64(fwd);
+    __syncwarp();
+    if (MBE_STATS_ON && lane == 0) WACC(ab_list) += 4ull * fwd;
+  }
+#endif
 
   if (MBE_STATS_ON && lane == 0) tsub[1] = (unsigned long long)clock64() - tph;
   MBE_PHASE(7, tph);
@@ -1481,8 +1558,17 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       w.skey[idx] = order_key(p.order, c, v, nLp);
       w.sval[idx] = idx;
       if (bm) {
+#if MBE_EXW_UNROLL
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          if (q < Wc) w.pbuf[(size_t)idx * Wc + q] = rw[q];
+#pragma unroll
+        for (uint32_t q = 0; q < MBE_SEXT_WORDS; ++q)  // compile-time indices: exw stays in registers
+          if (q + 4 < Wc) w.pbuf[(size_t)idx * Wc + q + 4] = exw[q];
+#else
         for (uint32_t q = 0; q < Wc && q < 4; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
         for (uint32_t q = 4; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = exw[q - 4];
+#endif
       }
     }
     nPc += __popc(bp);
@@ -1490,8 +1576,17 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       uint32_t bq = __ballot_sync(FULLMASK, isQ);
       if (isQ) {
         uint32_t idx = nQc + __popc(bq & lanemask_lt());
+#if MBE_EXW_UNROLL
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+          if (q < Wc) w.qbuf[(size_t)idx * Wc + q] = rw[q];
+#pragma unroll
+        for (uint32_t q = 0; q < MBE_SEXT_WORDS; ++q)
+          if (q + 4 < Wc) w.qbuf[(size_t)idx * Wc + q + 4] = exw[q];
+#else
         for (uint32_t q = 0; q < Wc && q < 4; ++q) w.qbuf[(size_t)idx * Wc + q] = rw[q];
         for (uint32_t q = 4; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = exw[q - 4];
+#endif
       }
       nQc += __popc(bq);
       if (Wc > 4 && valid) {
@@ -1513,9 +1608,9 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   MBE_PHASE(8, tph);
   account_task(w, p, nonmax);
   if (lane == 0 && MBE_STATS_ON) {
-    w.list_tasks++;
+    WACC(list_tasks)++;
     // N(x) + reverse-scan adjacency incl. offsets + touched rows (+ frame L, P, R reads)
-    w.ab_list += 4ull * dx + 4ull * (visits + nLp) + 8ull * nt + 4ull * (nL + 2ull * nP + nR);
+    WACC(ab_list) += 4ull * dx + 4ull * (visits + nLp) + 8ull * nt + 4ull * (nL + 2ull * nP + nR);
   }
   if (nonmax) return;
 
@@ -1623,7 +1718,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       C[4] = nRp;
       C[5] = w.cur_root;
       *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-      if MBE_STATS_ON w.ab_write += 4ull * size;
+      if MBE_STATS_ON WACC(ab_write) += 4ull * size;
     }
     publish_frame(w, p, size, nT);
   }
@@ -1775,8 +1870,8 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     if MBE_STATS_ON {
       const uint32_t q1 = stats_r1_size(Wn, qbuf, nQc, w, p);
       if (lane == 0) {
-        w.bitmap_tasks++;
-        w.ab_bit += 4ull * Wn * (2ull + q1);
+        WACC(bitmap_tasks)++;
+        WACC(ab_bit) += 4ull * Wn * (2ull + q1);
       }
     }
     if (!dom) {
@@ -1859,7 +1954,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if MBE_STATS_ON w.ab_write += 4ull * size;
+    if MBE_STATS_ON WACC(ab_write) += 4ull * size;
   }
   publish_frame(w, p, size, nS);
   MBE_PHASE(14, tph);
@@ -1888,6 +1983,8 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   if (lane < (int)W) lx[lane] = Prow[(size_t)i * W + lane];
   __syncwarp();
   const uint32_t k = __reduce_add_sync(FULLMASK, lane < (int)W ? (uint32_t)__popc(lx[lane]) : 0u);
+  // nonzero words of row(x): only they can meet another row (scans below skip the rest)
+  const uint32_t nzw = __ballot_sync(FULLMASK, lane < (int)W && lx[lane] != 0u);
 
   if (F[0] & HDR_UNCHECKED) {
     // Step 3 deferred to the task: x is not maximal iff a Q-role row (frame Q rows and
@@ -1899,14 +1996,17 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
       if (t < nQ + i) {
         const uint32_t* r = t < nQ ? Qrow + (size_t)t * W : Prow + (size_t)(t - nQ) * W;
         sup = true;
-        for (uint32_t q = 0; q < W && sup; ++q) sup = (lx[q] & ~r[q]) == 0u;
+        for (uint32_t bb = nzw; bb && sup; bb &= bb - 1u) {
+          const uint32_t q = (uint32_t)(__ffs(bb) - 1);
+          sup = (lx[q] & ~r[q]) == 0u;
+        }
       }
       dom = __any_sync(FULLMASK, sup);
     }
     account_task(w, p, dom);
     if (lane == 0 && MBE_STATS_ON) {
-      w.bitmap_tasks++;
-      w.ab_bit += 4ull * W * (1ull + nP + nQ);
+      WACC(bitmap_tasks)++;
+      WACC(ab_bit) += 4ull * W * (1ull + nP + nQ);
     }
     if (dom) return;
   }
@@ -1922,7 +2022,10 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     uint32_t c = 0;
     if (valid) {
       const uint32_t* r = Prow + (size_t)j * W;
-      for (uint32_t q = 0; q < W; ++q) c += __popc(r[q] & lx[q]);
+      for (uint32_t bb = nzw; bb; bb &= bb - 1u) {
+        const uint32_t q = (uint32_t)(__ffs(bb) - 1);
+        c += __popc(r[q] & lx[q]);
+      }
     }
     const uint32_t v = valid ? Pid[j] : 0u;
     const bool isExp = valid && c == k;
@@ -1973,9 +2076,10 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     if (valid) {
       off = t < nQ ? (uint32_t)((Qrow - F) + (size_t)t * W) : (uint32_t)((Prow - F) + (size_t)(t - nQ) * W);
       const uint32_t* r = F + off;
-      uint32_t a = 0;
-      for (uint32_t q = 0; q < W; ++q) a |= r[q] & lx[q];
-      keep = a != 0u;
+      for (uint32_t bb = nzw; bb && !keep; bb &= bb - 1u) {  // first meeting word decides
+        const uint32_t q = (uint32_t)(__ffs(bb) - 1);
+        keep = (r[q] & lx[q]) != 0u;
+      }
     }
     const uint32_t bq = __ballot_sync(FULLMASK, keep);
     if (keep) w.qbuf[nQc + __popc(bq & lanemask_lt())] = off;
@@ -2041,7 +2145,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     C[4] = nRp;
     C[5] = w.cur_root;
     *reinterpret_cast<unsigned long long*>(C + 6) = sRp;
-    if MBE_STATS_ON w.ab_write += 4ull * size;
+    if MBE_STATS_ON WACC(ab_write) += 4ull * size;
   }
   publish_frame(w, p, size, nS);
   MBE_PHASE(14, tph);
@@ -2264,10 +2368,12 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
   w.sm = reinterpret_cast<WarpSmem*>(smem_raw) + wib;
   w.cur_root = 0;
   w.failed = false;
-  w.count = w.hash = w.tasks = w.pruned = w.steals = 0;
-  w.list_tasks = w.bitmap_tasks = w.frames = 0;
-  w.ab_list = w.ab_bit = w.ab_write = 0;
-  w.max_depth = 0;
+  if (MBE_ACC_SMEM == 0 || lane == 0) {
+    WACC(count) = WACC(hash) = WACC(tasks) = WACC(pruned) = WACC(steals) = 0;
+    WACC(list_tasks) = WACC(bitmap_tasks) = WACC(frames) = 0;
+    WACC(ab_list) = WACC(ab_bit) = WACC(ab_write) = 0;
+    WACC(max_depth) = 0;
+  }
   if (lane == 0) {
     for (int k = 0; k < 16; ++k) w.sm->ph[k] = 0;
     w.sm->fc_depth = -1;
@@ -2442,7 +2548,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         __syncwarp();
         if (lane == 0) {
           atomicAdd(&dsc->done, tend - ti);  // the victim no longer needs to wait for this range
-          w.steals += tend - ti;
+          WACC(steals) += tend - ti;
           if MBE_STATS_ON w.sm->ph[3] += clock64() - t0;
         }
         publish_frame(w, p, fsz, tend, ti);
@@ -2463,7 +2569,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       if ((++done_tasks & 255u) == 0u) atomicAdd(&p.gl->progress, 1ull);  // watchdog heartbeat
       if (kind != 2) atomicAdd(&dsc->done, 1u);
       if (kind == 1 && nxt != PEND_NONE) w.sm->pend[d] = (uint32_t)nxt;
-      if (kind == 3) w.steals++;
+      if (kind == 3) WACC(steals)++;
       if MBE_STATS_ON {
         const int ph = kind == 2 ? 0 : task_phase(F);
         const unsigned long long dt = clock64() - t0;
@@ -2494,11 +2600,11 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
   if (lane == 0) {
     if MBE_STATS_ON atomicAdd(&p.gl->exit_hist[min(63ull, (globaltimer_ns() - t_start) / 2000000ull)], 1ull);
     p.stamps[gw] = w.stamp;
-    atomicAdd(&p.gl->count, w.count);
-    atomicAdd(&p.gl->hash, w.hash);
-    atomicAdd(&p.gl->tasks, w.tasks);
-    atomicAdd(&p.gl->pruned, w.pruned);
-    atomicAdd(&p.gl->steals, w.steals);
+    atomicAdd(&p.gl->count, WACC(count));
+    atomicAdd(&p.gl->hash, WACC(hash));
+    atomicAdd(&p.gl->tasks, WACC(tasks));
+    atomicAdd(&p.gl->pruned, WACC(pruned));
+    atomicAdd(&p.gl->steals, WACC(steals));
     if (roots) atomicAdd(&p.gl->roots_run, roots);
     if MBE_STATS_ON {
       // per-warp workload distribution (Fig. 5 analog): task cycles vs cycles until this warp exits
@@ -2508,14 +2614,14 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       atomicAdd(&p.gl->warp_busy_sum, busy);
       atomicMin(&p.gl->warp_busy_min, busy);
       atomicMax(&p.gl->warp_busy_max, busy);
-      atomicAdd(&p.gl->list_tasks, w.list_tasks);
-      atomicAdd(&p.gl->bitmap_tasks, w.bitmap_tasks);
-      atomicAdd(&p.gl->frames, w.frames);
-      atomicAdd(&p.gl->alg_bytes, w.ab_list + w.ab_bit + w.ab_write);
-      atomicAdd(&p.gl->alg_list, w.ab_list);
-      atomicAdd(&p.gl->alg_bitrow, w.ab_bit);
-      atomicAdd(&p.gl->alg_write, w.ab_write);
-      atomicMax(&p.gl->max_depth, w.max_depth);
+      atomicAdd(&p.gl->list_tasks, WACC(list_tasks));
+      atomicAdd(&p.gl->bitmap_tasks, WACC(bitmap_tasks));
+      atomicAdd(&p.gl->frames, WACC(frames));
+      atomicAdd(&p.gl->alg_bytes, WACC(ab_list) + WACC(ab_bit) + WACC(ab_write));
+      atomicAdd(&p.gl->alg_list, WACC(ab_list));
+      atomicAdd(&p.gl->alg_bitrow, WACC(ab_bit));
+      atomicAdd(&p.gl->alg_write, WACC(ab_write));
+      atomicMax(&p.gl->max_depth, WACC(max_depth));
       for (int k = 0; k < 16; ++k) atomicAdd(&p.gl->phase[k], w.sm->ph[k]);
     }
   }

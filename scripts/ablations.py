@@ -7,7 +7,10 @@ P:655-731): every variant is result-invariant, so each run is also a parity chec
 Variants: the default; bit-row threshold T = 256 / 128 / 32 (T = 32 leaves every frame with |L| > 32 on
 the reverse-scan list path, the closest to the paper's compact-array design); stealing off (paper: no
 WS); steal-half instead of single-task steals; antichain reduction of Q' off; root twin pruning off; the larger
-side as the candidate side (orientation, reading Z4); fewer resident warps (2 CTAs/SM).
+side as the candidate side (orientation, reading Z4); fewer resident warps (2 CTAs/SM); the paper's noRS
+(counts by forward intersection instead of reverse scanning); candidate order input /
+descending instead of the iMBE ascending order (these change the search tree, so their task
+count is reported, not compared).
 """
 import argparse
 import json
@@ -17,7 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2401_05039_b200 import (MBE_NO_ANTICHAIN, MBE_NO_STEAL, MBE_NO_TWIN,  # noqa: E402
+from paper_2401_05039_b200 import (MBE_NO_ANTICHAIN, MBE_NO_RS, MBE_NO_STEAL, MBE_NO_TWIN,  # noqa: E402
                                    MBE_STEAL_HALF, MBEGraph)
 from paper_2401_05039_b200 import inputs as I  # noqa: E402
 
@@ -32,6 +35,9 @@ VARIANTS = [
     ("no root twin pruning", dict(flags=MBE_NO_TWIN)),
     ("larger side as candidates", dict(candidate_side=-1)),
     ("2 CTAs/SM (8 warps/SM)", dict(ctas_per_sm=2)),
+    ("noRS: forward-intersection counts (P:691)", dict(flags=MBE_NO_RS)),
+    ("order: descending (-|N(v) ∩ L|, r)", dict(order="descending")),
+    ("order: input (original id)", dict(order="input")),
 ]
 
 
@@ -65,6 +71,8 @@ def main():
                     if max(g.n1, g.n2) > 200000:  # per-warp slot tables scale with the candidate side
                         continue
                     kw["candidate_side"] = 3 - smaller
+                if kw.get("order") == "input" and c != "C2":
+                    continue  # input order inflates the tree ~22x: C2 only
                 G.enumerate(**kw)  # warm-up (and the other side's ingest, if any)
                 times, r = [], None
                 for _ in range(a.reps):
@@ -74,7 +82,7 @@ def main():
                 want = gold.get(c)
                 exact = want is None or (r.count, r.hash) == want[:2]
                 same_tree = want is None or r.tasks == want[2] or kw.get("candidate_side") or \
-                    (kw.get("flags", 0) & MBE_NO_TWIN)
+                    (kw.get("flags", 0) & MBE_NO_TWIN) or kw.get("order")
                 if base is None:
                     base = ms
                 row = dict(config=c, variant=name, kernel_ms=[round(t, 2) for t in times], best_ms=round(ms, 2),
