@@ -53,6 +53,9 @@
 #ifndef MBE_SCAN_MLP
 #define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
 #endif
+#ifndef MBE_BACKOFF_MIN
+#define MBE_BACKOFF_MIN 64  // ns: first idle back-off after a failed steal attempt
+#endif
 #ifndef MBE_BACKOFF_MAX
 #define MBE_BACKOFF_MAX 32768  // ns: cap of an idle warp's exponential back-off between steal attempts
 #endif
@@ -2389,7 +2392,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
   bool roots_done = false;
   bool registered = false;
   bool ever_idle = false;
-  uint32_t backoff = 64;
+  uint32_t backoff = MBE_BACKOFF_MIN;
   uint32_t rot = 0;
 
   while (!w.failed) {
@@ -2529,7 +2532,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         if (lane == 0 && MBE_STATS_ON) w.sm->ph[4] += clock64() - t1;
         continue;
       }
-      backoff = 64;
+      backoff = MBE_BACKOFF_MIN;
       registered = false;
       __threadfence();  // acquire: the victim published the frame before its claim word
       if (lane == 0) dbg_delay(6);

@@ -71,8 +71,8 @@ def main():
                     if max(g.n1, g.n2) > 200000:  # per-warp slot tables scale with the candidate side
                         continue
                     kw["candidate_side"] = 3 - smaller
-                if kw.get("order") == "input" and c != "C2":
-                    continue  # input order inflates the tree ~22x: C2 only
+                if kw.get("order") and c != "C2":
+                    continue  # the order ablations inflate the tree 21x (input) / 82x (descending) on C2: C2 only
                 G.enumerate(**kw)  # warm-up (and the other side's ingest, if any)
                 times, r = [], None
                 for _ in range(a.reps):
