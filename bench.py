@@ -425,6 +425,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOADS.get(args.config, args.config), "count": count, "hash": f"{h:#018x}",
                        "candidate_side": st.candidate_side, "warps_per_gpu": st.n_warps,
+                       "workspace_gb": round(st.workspace_bytes / 1e9, 2),
                        "l2": "256 MiB buffer written between timed steps (graph fits in L2)",
                        "parallelism": (f"{world} rank(s) on {min(world, ndev)} GPU(s); level-1 subtrees "
                                        + ("claimed in guided-self-scheduling chunks from rank 0's IPC counter"

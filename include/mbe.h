@@ -162,6 +162,8 @@ typedef struct {
    * list tasks 4 deg(x) + 4 Σ_{u∈L'}(deg(u)+1) + 8 |touched| + 4 (|L| + 2|P| + |R|); bit-row tasks
    * 4 W (1 + |P| + |Q|) over their frame's stored rows (|Q| R1-reduced); child frames 4 x words written. */
   uint64_t alg_bytes_list, alg_bytes_bitrow, alg_bytes_write;
+  uint64_t workspace_bytes;  /* device workspace of the launch (all warps): per warp the frame arena, the
+                                candidate buffers sized by max_x |N(N(x))| and the two vertex-indexed tables */
 } mbe_result;
 
 /* Enumerate all maximal bicliques of g.  cfg NULL = defaults; res must be

@@ -54,7 +54,8 @@ class mbe_result(ctypes.Structure):
                 ("max_task_cycles", _u64 * 3), ("roots_out_ms", _dbl), ("max_phase_cycles", _u64 * 16),
                 ("roots_claimed", _u64), ("claim_chunks", _u32), ("attempts", _u32), ("busy_hist", _u32 * 20),
                 ("busy_ms_min", _dbl), ("busy_ms_mean", _dbl), ("busy_ms_max", _dbl),
-                ("alg_bytes_list", _u64), ("alg_bytes_bitrow", _u64), ("alg_bytes_write", _u64)]
+                ("alg_bytes_list", _u64), ("alg_bytes_bitrow", _u64), ("alg_bytes_write", _u64),
+                ("workspace_bytes", _u64)]
 
 
 class mbe_graph_info(ctypes.Structure):
@@ -149,6 +150,7 @@ class Result:
     busy_hist: tuple = ()
     busy_ms: tuple = ()  # (min, mean, max) task time per warp, MBE_STATS
     alg_parts: tuple = ()  # (list, bit-row, frame writes) algorithmic bytes, MBE_STATS
+    workspace_bytes: int = 0  # device workspace of the launch (all warps)
 
 
 def mbe_strerror(code: int) -> str:
@@ -213,7 +215,8 @@ def mbe_enumerate(handle: int, config: Optional[mbe_config] = None, output: Opti
                   float(res.roots_out_ms), tuple(int(v) for v in res.max_phase_cycles), int(res.roots_claimed),
                   int(res.claim_chunks), int(res.attempts), tuple(int(v) for v in res.busy_hist),
                   (float(res.busy_ms_min), float(res.busy_ms_mean), float(res.busy_ms_max)),
-                  (int(res.alg_bytes_list), int(res.alg_bytes_bitrow), int(res.alg_bytes_write)))
+                  (int(res.alg_bytes_list), int(res.alg_bytes_bitrow), int(res.alg_bytes_write)),
+                  int(res.workspace_bytes))
 
 
 def mbe_format_listing(output: mbe_output, n_records: int) -> bytes:

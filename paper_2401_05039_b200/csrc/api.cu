@@ -167,6 +167,7 @@ struct Side {
   bool twin_ready = false;      // root twin flags computed (graph-only, once per side)
   uint32_t auto_T = 0;          // cached auto bit-row threshold
   uint32_t nU = 0, nV = 0, n_roots = 0, maxdegU = 0;
+  uint64_t cand = 0;            // max |N(N(x))| over candidates x: bounds every task's candidate buffers
   std::vector<uint32_t> origU;  // host copy: rank -> original id
   std::vector<uint32_t> rankU;  // host copy: original id -> rank
   DevBuf all;                   // one device allocation holding every array below
@@ -237,7 +238,7 @@ struct Workspace {
   int device = 0;
   bool busy = false, dirty = true;
   uint32_t n_warps = 0, wmax = 0;
-  uint64_t cap_nU = 0, cap_lbuf = 0, arena_bytes = 0, stride = 0;
+  uint64_t cap_nU = 0, cap_cand = 0, cap_lbuf = 0, arena_bytes = 0, stride = 0;
   uint64_t o_slot = 0, o_sext = 0, o_touched = 0, o_lbuf = 0, o_rbuf = 0, o_skey = 0, o_sval = 0, o_pbuf = 0, o_qbuf = 0,
            o_arena = 0;
   DevBuf ws, desc, tops, stamps, hint, per_root, gl;
@@ -340,19 +341,48 @@ int build_side(mbe_graph* g, int s, uint32_t order = 0) {
   // execution-order cost of each level-1 subtree (descending P-role 2-hop estimate):
   //   cost(x) = Σ_{u ∈ N(x)} |{w ∈ N(u) : w > x}| = Σ_{u ∈ N(x)} deg(u) - k - 1, k = position of x in adjV[u]
   lap("adjacency: adjV");
-  std::vector<uint64_t> rcost(nU, 0);
+  std::vector<uint64_t> rcost(nU, 0), vis(nU, 0);
   parallel_edges(offU.data(), nU, nth, [&](unsigned, uint64_t a, uint64_t b) {
     for (uint64_t r = a; r < b; ++r) {
-      uint64_t c = 0;
+      uint64_t c = 0, v = 0;
       for (uint32_t e = offU[r]; e < offU[r + 1]; ++e) {
         const uint32_t u = adjU[e];
         const uint32_t k = (uint32_t)(std::lower_bound(adjV.begin() + offV[u], adjV.begin() + offV[u + 1], (uint32_t)r) -
                                       adjV.begin());
         c += offV[u + 1] - k - 1;
+        v += offV[u + 1] - offV[u];
       }
       rcost[r] = c;
+      vis[r] = v;
     }
   });
+  // Candidate-buffer bound: the largest 2-hop set |N(N(x))| (x included).  Every vertex a task in x's
+  // level-1 subtree touches, classifies or keeps as a P'/Q' row lies in N(N(x)) (L' ⊆ N(x) below the
+  // root), so it bounds the per-warp touched list, R', sort keys and P'/Q' rows.  |N(N(x))| <= vis(x) =
+  // Σ_{u ∈ N(x)} deg(u), so exact sizes are computed only for candidates, by descending vis, while vis
+  // can still beat the best found (a few dozen on power-law graphs).
+  {
+    std::vector<std::pair<uint64_t, uint32_t>> heap;
+    heap.reserve(nU);
+    for (uint32_t r = 0; r < nU; ++r) heap.emplace_back(vis[r], r);
+    std::make_heap(heap.begin(), heap.end());
+    std::vector<uint32_t> stamp(nU, 0xffffffffu);
+    uint64_t best = 0;
+    while (!heap.empty() && heap.front().first > best) {
+      const uint32_t r = heap.front().second;
+      std::pop_heap(heap.begin(), heap.end());
+      heap.pop_back();
+      uint64_t two = 0;
+      for (uint32_t e = offU[r]; e < offU[r + 1]; ++e)
+        for (uint32_t f = offV[adjU[e]]; f < offV[adjU[e] + 1]; ++f)
+          if (stamp[adjV[f]] != r) {
+            stamp[adjV[f]] = r;
+            ++two;
+          }
+      best = std::max(best, two);
+    }
+    S.cand = best;
+  }
   lap("adjacency");
   // hash terms: side bit 0 for side 1 (rows), 1 for side 2 (cols)
   std::vector<uint64_t> hvU(nU), hvV(nV);
@@ -410,32 +440,48 @@ int build_side(mbe_graph* g, int s, uint32_t order = 0) {
 
 uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
-// Per-warp workspace bytes (same layout as checkout_workspace).
-uint64_t workspace_stride(uint64_t nU, uint64_t maxdeg, uint64_t arena_bytes, uint32_t wmax) {
+// Per-warp workspace layout (bytes from the warp's base).  The hot, small-index parts of every scratch
+// buffer sit next to each other (arena first, then the candidate-indexed buffers), and the two
+// vertex-indexed tables (slot, sext: random access by vertex id) come last.  `cand` bounds the rows of any
+// one task's candidate buffers (touched, R', sort keys, P'/Q' rows).
+struct WsLayout {
+  uint64_t slot, sext, touched, lbuf, rbuf, skey, sval, pbuf, qbuf, arena, stride;
+};
+WsLayout ws_layout(uint64_t nU, uint64_t cand, uint64_t maxdeg, uint64_t arena_bytes, uint32_t wmax) {
   nU = std::max<uint64_t>(nU, 1);
+  cand = std::max<uint64_t>(std::min(cand, nU), 1);
   const uint64_t lb = std::max<uint64_t>(maxdeg, 32 * MBE_WMAX);
-  uint64_t o = align256(nU * 4 * MBE_SLOT_WORDS);
-  o = align256(o + nU * 4 * MBE_SEXT_WORDS);
-  o = align256(o + nU * 4);
-  o = align256(o + lb * 4);
-  o = align256(o + nU * 4);
-  o = align256(o + nU * 16);
-  o = align256(o + nU * 8);
-  o = align256(o + nU * wmax * 4);
-  o = align256(o + nU * wmax * 4);
-  return align256(o + arena_bytes);
+  WsLayout L;
+  uint64_t o = 0;
+  L.arena = o; o = align256(o + arena_bytes);
+  L.touched = o; o = align256(o + cand * 4);
+  L.lbuf = o; o = align256(o + lb * 4);
+  L.rbuf = o; o = align256(o + cand * 4);
+  L.skey = o; o = align256(o + cand * 32);  // sort keys + ping-pong copy, or a dedup hash table of <= 4 cand u64
+  L.sval = o; o = align256(o + cand * 8);
+  L.pbuf = o; o = align256(o + cand * wmax * 4);
+  L.qbuf = o; o = align256(o + cand * wmax * 4);
+  L.slot = o; o = align256(o + nU * 4 * MBE_SLOT_WORDS);
+  L.sext = o; o = align256(o + nU * 4 * MBE_SEXT_WORDS);
+  L.stride = o;
+  return L;
+}
+
+uint64_t workspace_stride(uint64_t nU, uint64_t cand, uint64_t maxdeg, uint64_t arena_bytes, uint32_t wmax) {
+  return ws_layout(nU, cand, maxdeg, arena_bytes, wmax).stride;
 }
 
 // Check out a workspace able to run n_warps warps over nU candidate vertices.
-int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t maxdeg, uint64_t arena_bytes,
+int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t cand, uint64_t maxdeg, uint64_t arena_bytes,
                        uint32_t wmax, Workspace** out) {
   nU = std::max<uint64_t>(nU, 1);
+  cand = std::max<uint64_t>(std::min(cand, nU), 1);
   const uint64_t lb = std::max<uint64_t>(maxdeg, 32 * MBE_WMAX);
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     for (Workspace* w : g_pool)
-      if (!w->busy && w->device == device && w->n_warps == n_warps && w->cap_nU >= nU && w->cap_lbuf >= lb &&
-          w->arena_bytes == arena_bytes && w->wmax >= wmax) {
+      if (!w->busy && w->device == device && w->n_warps == n_warps && w->cap_nU >= nU && w->cap_cand >= cand &&
+          w->cap_lbuf >= lb && w->arena_bytes == arena_bytes && w->wmax >= wmax) {
         w->busy = true;
         *out = w;
         return MBE_OK;
@@ -446,20 +492,22 @@ int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t maxde
   w->n_warps = n_warps;
   w->wmax = wmax;
   w->cap_nU = nU;
+  w->cap_cand = cand;
   w->cap_lbuf = lb;
   w->arena_bytes = arena_bytes;
-  uint64_t o = 0;
-  w->o_slot = o; o = align256(o + nU * 4 * MBE_SLOT_WORDS);
-  w->o_sext = o; o = align256(o + nU * 4 * MBE_SEXT_WORDS);
-  w->o_touched = o; o = align256(o + nU * 4);
-  w->o_lbuf = o; o = align256(o + lb * 4);
-  w->o_rbuf = o; o = align256(o + nU * 4);
-  w->o_skey = o; o = align256(o + nU * 16);
-  w->o_sval = o; o = align256(o + nU * 8);
-  w->o_pbuf = o; o = align256(o + nU * wmax * 4);
-  w->o_qbuf = o; o = align256(o + nU * wmax * 4);
-  w->o_arena = o; o = align256(o + arena_bytes);
-  w->stride = o;
+  const WsLayout L = ws_layout(nU, cand, maxdeg, arena_bytes, wmax);
+  w->o_slot = L.slot;
+  w->o_sext = L.sext;
+  w->o_touched = L.touched;
+  w->o_lbuf = L.lbuf;
+  w->o_rbuf = L.rbuf;
+  w->o_skey = L.skey;
+  w->o_sval = L.sval;
+  w->o_pbuf = L.pbuf;
+  w->o_qbuf = L.qbuf;
+  w->o_arena = L.arena;
+  w->stride = L.stride;
+  const uint64_t o = L.stride;
   const uint64_t total = o * n_warps;
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (cudaMalloc(&w->ws.p, total) == cudaSuccess) break;
@@ -510,7 +558,7 @@ void checkin_workspace(Workspace* w) {
 
 // zero the per-vertex slots (required invariant: zero between tasks) and the tag stamps
 int clear_tables(Workspace* w, cudaStream_t st) {
-  CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(w->ws.p) + w->o_slot, w->stride, 0, w->o_touched - w->o_slot,
+  CUDA_TRY(cudaMemset2DAsync(static_cast<uint8_t*>(w->ws.p) + w->o_slot, w->stride, 0, w->stride - w->o_slot,
                              w->n_warps, st));
   CUDA_TRY(cudaMemsetAsync(w->stamps.p, 0, 4ull * w->n_warps, st));
   w->dirty = false;
@@ -740,7 +788,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     }
     T = 128;
     for (uint32_t t : {512u, 256u}) {
-      if ((double)workspace_stride(S.nU, S.maxdegU, arena, mbe_words_for(t)) * n_warps <= 0.8 * (double)(fr + pooled)) {
+      if ((double)workspace_stride(S.nU, S.cand, S.maxdegU, arena, mbe_words_for(t)) * n_warps <= 0.8 * (double)(fr + pooled)) {
         T = t;
         break;
       }
@@ -809,12 +857,12 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     }
     const auto tw0 = std::chrono::steady_clock::now();
     if (!wg.w) {
-      rc = checkout_workspace(g->device, n_warps, S.nU, S.maxdegU, arena, wmax, &wg.w);
+      rc = checkout_workspace(g->device, n_warps, S.nU, S.cand, S.maxdegU, arena, wmax, &wg.w);
       // auto threshold: narrower rows when the device is shared (e.g. several ranks on one GPU)
       while (rc == MBE_ENOMEM && auto_T && T > 128) {
         T /= 2;
         wmax = mbe_words_for(T);
-        rc = checkout_workspace(g->device, n_warps, S.nU, S.maxdegU, arena, wmax, &wg.w);
+        rc = checkout_workspace(g->device, n_warps, S.nU, S.cand, S.maxdegU, arena, wmax, &wg.w);
       }
       if (rc) return rc;
     }
@@ -868,7 +916,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.o_pbuf = W->o_pbuf;
     p.o_qbuf = W->o_qbuf;
     p.o_arena = W->o_arena;
-    p.skey2_off = W->cap_nU;
+    p.skey2_off = W->cap_cand;
     p.arena_words = arena / 4;
     p.desc = static_cast<Desc*>(W->desc.p);
     p.tops = static_cast<unsigned int*>(W->tops.p);
@@ -883,6 +931,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.rec_n2 = (unsigned int*)lb.n2.p;
     p.out_ids = (unsigned int*)lb.ids.p;
 
+    res->workspace_bytes = W->ws.bytes;
     Globals* dgl = static_cast<Globals*>(W->gl.p);
     CUDA_TRY(cudaMemsetAsync(dgl, 0, want_stats ? sizeof(Globals) : MBE_GLOBALS_HOT_BYTES, st));
     if (want_stats) {

@@ -1658,10 +1658,10 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     uint32_t qn = nQc;
     const unsigned long long td0 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
     if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
-      // hash table in the (now free) sort-key scratch: 2 x nU u64 entries, power of two >= 2 nQc
+      // hash table in the (now free) sort-key scratch: 4 x cand u64 entries, power of two >= 2 nQc
       uint32_t lg = 1;
       while ((1u << lg) < 2 * nQc) ++lg;
-      if ((1ull << lg) <= 2ull * p.skey2_off) {
+      if ((1ull << lg) <= 4ull * p.skey2_off) {
         qn = dedup_hash_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, lg, lane);
       } else {
         qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
