@@ -3,7 +3,9 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef MBE_MAXDEPTH
 #define MBE_MAXDEPTH 48    // per-warp stack depth (search depth is 7-11 on C2-C5)
+#endif
 #define MBE_WMAX 16        // bit rows of up to 16 x 32 = 512 columns
 #define MBE_SLOT_WORDS 8   // per-vertex scratch slot: count, -, tag (2), bit row words 0-3 = one 32-B sector
 #define MBE_SEXT_WORDS 12  // per-vertex extension: bit row words 4-15 (wide rows only)

@@ -89,7 +89,7 @@ namespace {
 #define FC_WORDS 256  // shared-memory copy of the warp's top frame (owner reads only)
 #endif
 #ifndef MBE_ACC_SMEM
-#define MBE_ACC_SMEM 0  // 1: lane-0 result accumulators in shared memory instead of registers
+#define MBE_ACC_SMEM 1  // lane-0 result accumulators in shared memory (frees registers: fewer spills on the task path)
 #endif
 #if MBE_ACC_SMEM
 #define WACC(f) (w.sm->a_##f)
@@ -115,6 +115,7 @@ struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligne
   unsigned int lx[MBE_WMAX];         // row(x) of a wide (8/16-word) bit-row task
   int fc_depth;                      // depth held in fcache, -1 = none
   int pad_[3];
+  unsigned long long wd_seen, wd_since;  // no-progress watchdog state (lane 0)
   union __align__(16) {
     unsigned short posv[32 * MBE_WMAX];  // wide tasks: column positions of row(x)'s set bits
     struct {                             // narrow tasks with small candidate bounds:
@@ -125,7 +126,7 @@ struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligne
   unsigned int lbuf[128];            // L' ids
   unsigned int rbuf[SM_RBUF];        // expanded R' vertices
 #if MBE_ACC_SMEM
-  // lane-0 result accumulators (in shared memory instead of registers; measured slower, off)
+  // lane-0 result accumulators (MBE_ACC_SMEM)
   unsigned long long a_count, a_hash, a_tasks, a_pruned, a_steals, a_list_tasks, a_bitmap_tasks, a_frames;
   unsigned long long a_ab_list, a_ab_bit, a_ab_write;
   unsigned int a_max_depth, a_pad;
@@ -137,20 +138,12 @@ struct __align__(16) WarpSmem {  // every array below starts at a 16-byte aligne
 struct Warp {
   int lane;
   uint32_t gw;
-  uint32_t* slot;  // [nU][MBE_SLOT_WORDS]: cnt, -, tag lo, tag hi, bit row words 0-3 (one 32-B sector)
-  uint32_t* sext;  // [nU][MBE_SEXT_WORDS]: bit row words 4-15 (wide rows)
-  uint32_t* touched;
-  uint32_t* lbuf;
-  uint32_t* rbuf;
-  unsigned long long* skey;
-  uint32_t* sval;
-  uint32_t* pbuf;
-  uint32_t* qbuf;
-  uint32_t* arena;
-  uint64_t arena_words;
+  // per-warp workspace base: the buffers are WB(slot), WB(touched), ... = base + the launch's offsets
+  // (kernel-parameter constants), so no pointer per buffer stays live across the task code
+  uint8_t* base;
   Desc* desc;
   uint32_t top;
-  uint64_t atop;
+  uint32_t atop;  // arena word offset of the next frame (Desc.off is 32-bit)
   uint32_t stamp;
   WarpSmem* sm;
   uint32_t cur_root;
@@ -162,6 +155,21 @@ struct Warp {
   uint32_t max_depth;
 #endif
 };
+
+// Per-warp buffers (api.cu ws_layout): slot [nU][MBE_SLOT_WORDS] (count, -, tag lo, tag hi, bit row words
+// 0-3: one 32-B sector), sext [nU][MBE_SEXT_WORDS] (bit row words 4-15), touched, lbuf, rbuf, skey, sval,
+// pbuf, qbuf (candidate-indexed) and the frame arena.
+#define WB_T_slot uint32_t
+#define WB_T_sext uint32_t
+#define WB_T_touched uint32_t
+#define WB_T_lbuf uint32_t
+#define WB_T_rbuf uint32_t
+#define WB_T_skey unsigned long long
+#define WB_T_sval uint32_t
+#define WB_T_pbuf uint32_t
+#define WB_T_qbuf uint32_t
+#define WB_T_arena uint32_t
+#define WB(f) (reinterpret_cast<WB_T_##f*>(w.base + p.o_##f))
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
@@ -456,16 +464,16 @@ __device__ __noinline__ void sort_pairs_small(unsigned long long* key, uint32_t*
 __device__ void warp_sort_pairs(Warp& w, const SearchParams& p, uint32_t n, uint32_t max_count) {
   if (n <= 1) return;
   if (n <= 32) {
-    sort_regs32(w.skey, w.sval, n, w.lane);
+    sort_regs32(WB(skey), WB(sval), n, w.lane);
   } else if (n <= MBE_SMEM_SORT) {
-    sort_smem(w.skey, w.sval, n, w.sm, w.lane);
+    sort_smem(WB(skey), WB(sval), n, w.sm, w.lane);
   } else {
     // second buffers live right after the first ones (same per-warp region, sized nU)
-    unsigned long long* key2 = w.skey + p.skey2_off;
-    uint32_t* val2 = w.sval + p.skey2_off;
+    unsigned long long* key2 = WB(skey) + p.skey2_off;
+    uint32_t* val2 = WB(sval) + p.skey2_off;
     const uint32_t ib = bit_length(p.g.nU), cb = bit_length(max_count);
-    if (p.order == 1u) sort_radix(w.skey, w.sval, key2, val2, n, cb, ib, w.sm, w.lane);
-    else sort_radix(w.skey, w.sval, key2, val2, n, ib, cb, w.sm, w.lane);
+    if (p.order == 1u) sort_radix(WB(skey), WB(sval), key2, val2, n, cb, ib, w.sm, w.lane);
+    else sort_radix(WB(skey), WB(sval), key2, val2, n, ib, cb, w.sm, w.lane);
   }
 }
 
@@ -656,6 +664,53 @@ __device__ __noinline__ uint32_t dedup_hash_rows(const uint32_t* src, uint32_t n
   }
   __syncwarp();
   return m;
+}
+
+// R1 pre-filter (exact, O(n · popcount)): champ[c] = the row of largest popcount (lowest index on ties)
+// having column c.  A row contained in the champion of one of its columns is dropped: a strictly contained
+// row is dominated, an equal row is a later copy of the champion.  Every distinct maximal row keeps a copy,
+// so the antichain of the survivors is the antichain of all n rows; most rows of a hub's Q' (a handful of
+// columns each) go here instead of through the O(n · K) pass.  W <= 8 words, k <= 32 W columns, n < 2^22.
+#ifndef MBE_CHAMP_MIN
+#define MBE_CHAMP_MIN 128u  // list-path Q' candidate sets above this go through the champion filter (0: off)
+#endif
+#define CHAMP_IDX 0x3FFFFFu
+__device__ __noinline__ uint32_t champion_filter(const uint32_t* src, uint32_t n, uint32_t W, uint32_t k, uint32_t* dst,
+                                                 uint32_t* champ, int lane) {
+  for (uint32_t c = lane; c < k; c += 32) champ[c] = 0u;
+  __syncwarp();
+  for (uint32_t t = lane; t < n; t += 32) {
+    const uint32_t* r = src + (size_t)t * W;
+    uint32_t pc = 0;
+    for (uint32_t q = 0; q < W; ++q) pc += __popc(r[q]);
+    const uint32_t key = (pc << 22) | (CHAMP_IDX - t);
+    for (uint32_t q = 0; q < W; ++q)
+      for (uint32_t m = r[q]; m; m &= m - 1u) atomicMax(&champ[32 * q + __ffs(m) - 1], key);
+  }
+  __syncwarp();
+  uint32_t out = 0;
+  for (uint32_t base = 0; base < n; base += 32) {
+    const uint32_t t = base + lane;
+    bool keep = t < n;
+    const uint32_t* r = src + (size_t)(keep ? t : 0u) * W;
+    for (uint32_t q = 0, seen = 0; q < W && keep && seen < 8; ++q)
+      for (uint32_t m = r[q]; m && keep && seen < 8; m &= m - 1u, ++seen) {
+        const uint32_t j = CHAMP_IDX - (champ[32 * q + __ffs(m) - 1] & CHAMP_IDX);
+        if (j == t) continue;
+        const uint32_t* o = src + (size_t)j * W;
+        uint32_t x = 0;
+        for (uint32_t qq = 0; qq < W; ++qq) x |= r[qq] & ~o[qq];
+        if (x == 0u) keep = false;
+      }
+    const uint32_t bk = __ballot_sync(FULLMASK, keep);
+    if (keep) {
+      uint32_t* d = dst + (size_t)(out + __popc(bk & lanemask_lt())) * W;
+      for (uint32_t q = 0; q < W; ++q) d[q] = r[q];
+    }
+    out += __popc(bk);
+  }
+  __syncwarp();
+  return out;
 }
 
 // Same reduction for wide rows (8 or 16 words), word-sliced: rows are streamed from
@@ -966,7 +1021,7 @@ __device__ __noinline__ void write_record(const int lane, const SearchParams& p,
 
 // Reserve space for a child frame at the top of the arena; false on overflow.
 __device__ __forceinline__ bool arena_reserve(Warp& w, const SearchParams& p, uint64_t words) {
-  if (w.atop + words + 8 > w.arena_words || w.top + 1 >= MBE_MAXDEPTH) {
+  if (w.atop + words + 8 > p.arena_words || w.top + 1 >= MBE_MAXDEPTH) {
     if (w.lane == 0) set_error(p, w.top + 1 >= MBE_MAXDEPTH ? 2u : 1u, w.atop + words);
     w.failed = true;
     return false;
@@ -1112,20 +1167,24 @@ __device__ __forceinline__ bool prune_q_rows(const Row<W>& r, bool alive, const 
   return alive;
 }
 
-// Row t (ascending key order) is Pr[perm[t]] (perm == nullptr: Pr[t]).
+// Row t (ascending key order) is Pr[perm[t] & PERM_IDX] (perm == nullptr: Pr[t]); a set PERM_QDOM bit
+// marks a row already found inside a Q' row (prune_q_mark), so the Q scan is skipped (pass nQ = 0).
+#define PERM_QDOM 0x80000000u
+#define PERM_IDX 0x7fffffffu
 template <int W>
 __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t* perm, uint32_t nP, const uint32_t* Qr,
                                              uint32_t nQ, uint32_t* S, int lane, bool ascending = true) {
   uint32_t nS = 0;
   for (uint32_t tb = 0; tb < nP; tb += 32) {
     const uint32_t t = tb + lane;
-    bool alive = t < nP;
-    const Row<W> r = alive ? load_row<W>(Pr + (size_t)(perm ? perm[t] : t) * W) : zero_row<W>();
+    const uint32_t pt = t < nP && perm ? perm[t] : t;
+    bool alive = t < nP && !(pt & PERM_QDOM);
+    const Row<W> r = alive ? load_row<W>(Pr + (size_t)(pt & PERM_IDX) * W) : zero_row<W>();
     uint32_t key = 0;
 #pragma unroll
     for (int q = 0; q < W; ++q) key += __popc(r.w[q]);
     for (int j = (int)t - 1; alive && j >= 0; --j) {
-      const Row<W> s = load_row<W>(Pr + (size_t)(perm ? perm[j] : (uint32_t)j) * W);
+      const Row<W> s = load_row<W>(Pr + (size_t)(perm ? perm[j] & PERM_IDX : (uint32_t)j) * W);
       if (!ascending) {  // order ablation: any earlier sibling may contain row t
         if (row_subset<W>(r, s)) alive = false;
         continue;
@@ -1143,6 +1202,24 @@ __device__ __noinline__ uint32_t prune_frame(const uint32_t* Pr, const uint32_t*
   }
   __syncwarp();
   return nS;
+}
+
+// Step 3's Q part on UNSORTED candidates (row idx = Pr[idx]): sets PERM_QDOM in val[idx] for every row
+// contained in a Q' row; returns how many are not.  Domination by Q' does not depend on the sibling
+// order, so a child whose candidates are all dominated needs no ordering and publishes nothing.
+template <int W>
+__device__ __noinline__ uint32_t prune_q_mark(const uint32_t* Pr, uint32_t* val, uint32_t nP, const uint32_t* Qr,
+                                              uint32_t nQ, int lane) {
+  uint32_t n = 0;
+  for (uint32_t tb = 0; tb < nP; tb += 32) {
+    const uint32_t t = tb + lane;
+    const Row<W> r = t < nP ? load_row<W>(Pr + (size_t)t * W) : zero_row<W>();
+    const bool alive = prune_q_rows<W>(r, t < nP, Qr, nQ);
+    if (t < nP && !alive) val[t] |= PERM_QDOM;
+    n += __popc(__ballot_sync(FULLMASK, alive));
+  }
+  __syncwarp();
+  return n;
 }
 
 // Wide rows (8/16 words): the same test word-sliced, rows read from memory (L1).  Every row's
@@ -1295,7 +1372,7 @@ __device__ __forceinline__ void account_children(Warp& w, const SearchParams& p,
 __device__ __noinline__ uint32_t stats_r1_size(uint32_t Wn, const uint32_t* src, uint32_t n, Warp& w,
                                                const SearchParams& p) {
   if (n == 0 || (uint64_t)n * Wn > 4ull * p.skey2_off) return n;
-  return antichain_w(Wn, src, n, reinterpret_cast<uint32_t*>(w.skey), false, w.lane, w.sm);
+  return antichain_w(Wn, src, n, reinterpret_cast<uint32_t*>(WB(skey)), false, w.lane, w.sm);
 }
 
 // ================================================================== list path
@@ -1343,8 +1420,8 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     Lp = Nx;
     nLp = dx;
   } else {
-    nLp = warp_intersect(L, nL, Nx, dx, w.lbuf, lane);
-    Lp = w.lbuf;
+    nLp = warp_intersect(L, nL, Nx, dx, WB(lbuf), lane);
+    Lp = WB(lbuf);
     if (nLp != key) {
       if (lane == 0) set_error(p, 3u, ((unsigned long long)nLp << 32) | key);
       w.failed = true;
@@ -1360,9 +1437,9 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     w.stamp++;
     const unsigned long long st = ((unsigned long long)w.stamp) << 32;
     for (uint32_t j = lane; j < nP; j += 32)
-      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)Pid[j] * MBE_SLOT_WORDS + 2) = st | (j + 1);
+      *reinterpret_cast<unsigned long long*>(WB(slot) + (size_t)Pid[j] * MBE_SLOT_WORDS + 2) = st | (j + 1);
     for (uint32_t j = lane; j < nR; j += 32)
-      *reinterpret_cast<unsigned long long*>(w.slot + (size_t)R[j] * MBE_SLOT_WORDS + 2) = st | TAG_R;
+      *reinterpret_cast<unsigned long long*>(WB(slot) + (size_t)R[j] * MBE_SLOT_WORDS + 2) = st | TAG_R;
     __syncwarp();
   }
 
@@ -1412,20 +1489,20 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
 #if MBE_INSTR
       if (p.flags & F_NO_RS) {  // noRS ablation: the scan only discovers the vertices (counts below)
 #pragma unroll
-        for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicExch(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
+        for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicExch(&WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
       } else
 #endif
       {
 #pragma unroll
-      for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicAdd(&w.slot[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
+      for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicAdd(&WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
       }
       if (bm && !(MBE_INSTR && (p.flags & F_NO_RS))) {
 #pragma unroll
         for (int j = 0; j < MBE_SCAN_MLP; ++j)
           if (fv[j]) {
             const uint32_t q = pos[j] >> 5;
-            uint32_t* wd = q < 4 ? &w.slot[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + q]
-                                 : &w.sext[(size_t)vv[j] * MBE_SEXT_WORDS + q - 4];
+            uint32_t* wd = q < 4 ? &WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + q]
+                                 : &WB(sext)[(size_t)vv[j] * MBE_SEXT_WORDS + q - 4];
             atomicOr(wd, 1u << (pos[j] & 31));
           }
       }
@@ -1433,7 +1510,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       for (int j = 0; j < MBE_SCAN_MLP; ++j) {
         bool isnew = old[j] == 0u;
         uint32_t b = __ballot_sync(FULLMASK, isnew);
-        if (isnew) w.touched[nt + __popc(b & lanemask_lt())] = vv[j];
+        if (isnew) WB(touched)[nt + __popc(b & lanemask_lt())] = vv[j];
         nt += __popc(b);
       }
     }
@@ -1447,7 +1524,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     // sorted L' (P:138-161 as written), and its bit row from the positions found
     unsigned long long fwd = 0;
     for (uint32_t t = lane; t < nt; t += 32) {
-      const uint32_t v = w.touched[t];
+      const uint32_t v = WB(touched)[t];
       const uint32_t* Nv = g.adjU + g.offU[v];
       const uint32_t dv = g.offU[v + 1] - g.offU[v];
       uint32_t c = 0;
@@ -1463,12 +1540,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
           ++c;
           if (bm) {
             const uint32_t q = lo >> 5;
-            uint32_t* wd = q < 4 ? &w.slot[(size_t)v * MBE_SLOT_WORDS + 4 + q] : &w.sext[(size_t)v * MBE_SEXT_WORDS + q - 4];
+            uint32_t* wd = q < 4 ? &WB(slot)[(size_t)v * MBE_SLOT_WORDS + 4 + q] : &WB(sext)[(size_t)v * MBE_SEXT_WORDS + q - 4];
             *wd |= 1u << (lo & 31);
           }
         }
       }
-      w.slot[(size_t)v * MBE_SLOT_WORDS] = c;
+      WB(slot)[(size_t)v * MBE_SLOT_WORDS] = c;
       fwd += dv;
     }
     fwd = warp_sum64(fwd);
@@ -1489,12 +1566,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
 #pragma unroll
     for (int j = 0; j < MBE_CLS_MLP; ++j) {
       uint32_t t = tb + 32 * j + lane;
-      vs[j] = t < nt ? w.touched[t] : 0xffffffffu;
+      vs[j] = t < nt ? WB(touched)[t] : 0xffffffffu;
     }
 #pragma unroll
     for (int j = 0; j < MBE_CLS_MLP; ++j) {
       if (vs[j] != 0xffffffffu) {
-        const uint4* sp = reinterpret_cast<const uint4*>(w.slot + (size_t)vs[j] * MBE_SLOT_WORDS);
+        const uint4* sp = reinterpret_cast<const uint4*>(WB(slot) + (size_t)vs[j] * MBE_SLOT_WORDS);
         sa[j] = sp[0];
         sb[j] = sp[1];
       } else {
@@ -1505,7 +1582,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
 #pragma unroll
     for (int j = 0; j < MBE_CLS_MLP; ++j) {
       if (vs[j] != 0xffffffffu) {
-        uint4* sp = reinterpret_cast<uint4*>(w.slot + (size_t)vs[j] * MBE_SLOT_WORDS);
+        uint4* sp = reinterpret_cast<uint4*>(WB(slot) + (size_t)vs[j] * MBE_SLOT_WORDS);
         sp[0] = make_uint4(0u, 0u, 0u, 0u);
         sp[1] = make_uint4(0u, 0u, 0u, 0u);
       }
@@ -1539,12 +1616,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     bool isPc = isP && c < nLp;
     if (isExp) sRx += g.hvU[v];
     uint32_t be = __ballot_sync(FULLMASK, isExp);
-    if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
+    if (isExp) WB(rbuf)[nRx + __popc(be & lanemask_lt())] = v;
     nRx += __popc(be);
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
     // words 4.. of a wide (8/16-word) row are still in the slot extension: staged in registers
     // with vector loads (one round trip), copied to the candidate buffers, then cleared
-    uint32_t* ex = w.sext + (size_t)v * MBE_SEXT_WORDS;
+    uint32_t* ex = WB(sext) + (size_t)v * MBE_SEXT_WORDS;
     uint32_t exw[MBE_SEXT_WORDS];
     if (Wc > 4 && valid) {
       const uint4* e4 = reinterpret_cast<const uint4*>(ex);
@@ -1558,19 +1635,19 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     }
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
-      w.skey[idx] = order_key(p.order, c, v, nLp);
-      w.sval[idx] = idx;
+      WB(skey)[idx] = order_key(p.order, c, v, nLp);
+      WB(sval)[idx] = idx;
       if (bm) {
 #if MBE_EXW_UNROLL
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q)
-          if (q < Wc) w.pbuf[(size_t)idx * Wc + q] = rw[q];
+          if (q < Wc) WB(pbuf)[(size_t)idx * Wc + q] = rw[q];
 #pragma unroll
         for (uint32_t q = 0; q < MBE_SEXT_WORDS; ++q)  // compile-time indices: exw stays in registers
-          if (q + 4 < Wc) w.pbuf[(size_t)idx * Wc + q + 4] = exw[q];
+          if (q + 4 < Wc) WB(pbuf)[(size_t)idx * Wc + q + 4] = exw[q];
 #else
-        for (uint32_t q = 0; q < Wc && q < 4; ++q) w.pbuf[(size_t)idx * Wc + q] = rw[q];
-        for (uint32_t q = 4; q < Wc; ++q) w.pbuf[(size_t)idx * Wc + q] = exw[q - 4];
+        for (uint32_t q = 0; q < Wc && q < 4; ++q) WB(pbuf)[(size_t)idx * Wc + q] = rw[q];
+        for (uint32_t q = 4; q < Wc; ++q) WB(pbuf)[(size_t)idx * Wc + q] = exw[q - 4];
 #endif
       }
     }
@@ -1582,13 +1659,13 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
 #if MBE_EXW_UNROLL
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q)
-          if (q < Wc) w.qbuf[(size_t)idx * Wc + q] = rw[q];
+          if (q < Wc) WB(qbuf)[(size_t)idx * Wc + q] = rw[q];
 #pragma unroll
         for (uint32_t q = 0; q < MBE_SEXT_WORDS; ++q)
-          if (q + 4 < Wc) w.qbuf[(size_t)idx * Wc + q + 4] = exw[q];
+          if (q + 4 < Wc) WB(qbuf)[(size_t)idx * Wc + q + 4] = exw[q];
 #else
-        for (uint32_t q = 0; q < Wc && q < 4; ++q) w.qbuf[(size_t)idx * Wc + q] = rw[q];
-        for (uint32_t q = 4; q < Wc; ++q) w.qbuf[(size_t)idx * Wc + q] = exw[q - 4];
+        for (uint32_t q = 0; q < Wc && q < 4; ++q) WB(qbuf)[(size_t)idx * Wc + q] = rw[q];
+        for (uint32_t q = 4; q < Wc; ++q) WB(qbuf)[(size_t)idx * Wc + q] = exw[q - 4];
 #endif
       }
       nQc += __popc(bq);
@@ -1620,7 +1697,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   const uint32_t nRp = nR + 1 + nRx;
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, nLp, sRp, nRp);
-  if (MBE_CAP_RECORDS) write_record(w.lane, p, Lp, nLp, R, nR, x, w.rbuf, nRx);
+  if (MBE_CAP_RECORDS) write_record(w.lane, p, Lp, nLp, R, nR, x, WB(rbuf), nRx);
   if (nPc == 0) return;
 
   // Child frame (L', R', P' sorted by (count, r), Q') at the arena top.  A wide (8/16-word)
@@ -1635,39 +1712,42 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
   const uint64_t need = MBE_HDR_WORDS + nLp + nRp + 4 + (cbm ? (uint64_t)nPc * (2 + Wc) + (uint64_t)nQc * Wc
                                                             : 2ull * nPc);
   if (!arena_reserve(w, p, need)) return;
-  uint32_t* C = w.arena + w.atop;
+  uint32_t* C = WB(arena) + w.atop;
   uint32_t* CL = C + MBE_HDR_WORDS;
   uint32_t* CR = CL + nLp;
   uint32_t* CP = CR + nRp;
   for (uint32_t t = lane; t < nLp; t += 32) CL[t] = Lp[t];
-  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
-  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, w.skey[t]);
+  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : WB(rbuf)[t - nR - 1]);
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, WB(skey)[t]);
   uint64_t size;
   uint32_t nQk = 0;
   uint32_t nT = nPc;  // tasks published (bit-row children: the survivors of the eager check)
   bool deferred = false;  // bit-row child published unchecked (HDR_UNCHECKED)
   if (cbm) {
-    uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
+    uint32_t* CPr = WB(arena) + align4(w.atop + (CP + nPc - C));
     for (uint32_t t = lane; t < nPc; t += 32) {
-      uint32_t src = w.sval[t];
-      for (uint32_t q = 0; q < Wc; ++q) CPr[(size_t)t * Wc + q] = w.pbuf[(size_t)src * Wc + q];
+      uint32_t src = WB(sval)[t];
+      for (uint32_t q = 0; q < Wc; ++q) CPr[(size_t)t * Wc + q] = WB(pbuf)[(size_t)src * Wc + q];
     }
     uint32_t* CQ = CPr + (size_t)nPc * Wc;
     __syncwarp();
-    const uint32_t* qsrc = w.qbuf;
+    const uint32_t* qsrc = WB(qbuf);
     uint32_t qn = nQc;
     const unsigned long long td0 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
-    if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
+    if (MBE_CHAMP_MIN && !(p.flags & F_NO_ANTICHAIN) && Wc <= 8 && nQc > MBE_CHAMP_MIN && nQc <= CHAMP_IDX) {
+      qn = champion_filter(WB(qbuf), nQc, Wc, nLp, WB(pbuf), w.sm->hist, lane);  // hist: 256 words >= nLp here
+      qsrc = WB(pbuf);
+    } else if (!(p.flags & F_NO_ANTICHAIN) && (nQc > p.dedup_min || (Wc >= 8 && nQc > 64))) {  // drop duplicates first
       // hash table in the (now free) sort-key scratch: 4 x cand u64 entries, power of two >= 2 nQc
       uint32_t lg = 1;
       while ((1u << lg) < 2 * nQc) ++lg;
       if ((1ull << lg) <= 4ull * p.skey2_off) {
-        qn = dedup_hash_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, lg, lane);
+        qn = dedup_hash_rows(WB(qbuf), nQc, Wc, WB(pbuf), WB(skey), lg, lane);
       } else {
-        qn = dedup_sort_rows(w.qbuf, nQc, Wc, w.pbuf, w.skey, w.sval, w.skey + p.skey2_off, w.sval + p.skey2_off,
+        qn = dedup_sort_rows(WB(qbuf), nQc, Wc, WB(pbuf), WB(skey), WB(sval), WB(skey) + p.skey2_off, WB(sval) + p.skey2_off,
                              w.sm, lane);
       }
-      qsrc = w.pbuf;
+      qsrc = WB(pbuf);
     }
     const unsigned long long td1 = MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
     // wide rows with many distinct Q' rows: keep the (exactly deduplicated) rows without the
@@ -1678,12 +1758,12 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
                           (qn > p.ac_min && qn > p.ac_ratio * (nPc + 1));
     bool sorted = false;
     if (!keep_all && Wc <= 4 && qn > 128) {  // descending popcount: the antichain needs no removal pass
-      uint32_t* tmp = qsrc == w.pbuf ? w.qbuf : w.pbuf;
+      uint32_t* tmp = qsrc == WB(pbuf) ? WB(qbuf) : WB(pbuf);
       popc_sort_rows_desc(qsrc, qn, Wc, tmp, w.sm->hist, lane);  // 32 Wc + 1 <= 129 bins
       qsrc = tmp;
       sorted = true;
     }
-    nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, w.skey, sorted);
+    nQk = antichain_w(Wc, qsrc, qn, CQ, keep_all, lane, w.sm, WB(skey), sorted);
     if MBE_STATS_ON {
       tdd[0] = td1 - td0;
       tdd[1] = (unsigned long long)clock64() - td1;
@@ -1699,7 +1779,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       for (uint32_t t = lane; t < nPc; t += 32) S[t] = t;
       nT = nPc;
     } else {
-      nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, w.skey, w.pbuf, lane, MBE_STATS_ON ? pprof : nullptr, p.order == 0u);
+      nT = prune_frame_w(Wc, CPr, nPc, CQ, nQk, S, WB(skey), WB(pbuf), lane, MBE_STATS_ON ? pprof : nullptr, p.order == 0u);
       account_children(w, p, nPc, nT, Wc, nQk);
     }
     if MBE_STATS_ON {
@@ -1709,7 +1789,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     size = (uint64_t)(S + nT - C);
   } else {
     uint32_t* CK = CP + nPc;
-    for (uint32_t t = lane; t < nPc; t += 32) CK[t] = key_count(p.order, w.skey[t], nLp);
+    for (uint32_t t = lane; t < nPc; t += 32) CK[t] = key_count(p.order, WB(skey)[t], nLp);
     size = (uint64_t)(CK + nPc - C);
   }
   if (nT > 0) {
@@ -1771,17 +1851,22 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
   // Step 4, expansion over P-role rows j > i.
   const uint32_t Wn = mbe_words_for(k);
   const MbeCompress<W> cmp = mbe_compress_prep_w<W>(Lx.w);
+  // 1-word rows: candidate rows are kept as r & row(x) in the frame's columns.  Inclusion, equality and
+  // popcount are the same as for the column-compressed rows (compression is a bijection on subsets of
+  // row(x)), so Step 3 and R1 decide on them directly; rows are compressed only when a child frame is
+  // written (most children are pruned entirely and never need it).
+  constexpr bool LAZY = (W == 1);
   uint32_t nPc = 0, nRx = 0, nQc = 0;
   unsigned long long sRx = 0;
   // scratch in shared memory when the candidate bounds fit (P' <= nP-i-1, Q' <= nQ+i)
   const uint32_t maxP = nP - i - 1, maxQ = nQ + i;
   const bool smP = maxP <= MBE_SMEM_SORT && maxP * Wn <= SM_PROW_WORDS && maxP <= SM_RBUF;
   const bool smQ = maxQ * Wn <= SM_QROW_WORDS;
-  unsigned long long* kbuf = smP ? w.sm->skey : w.skey;
-  uint32_t* vbuf = smP ? w.sm->sval : w.sval;
-  uint32_t* pbuf = smP ? w.sm->prow : w.pbuf;
-  uint32_t* rbuf = smP ? w.sm->rbuf : w.rbuf;
-  uint32_t* qbuf = smQ ? w.sm->qrow : w.qbuf;
+  unsigned long long* kbuf = smP ? w.sm->skey : WB(skey);
+  uint32_t* vbuf = smP ? w.sm->sval : WB(sval);
+  uint32_t* pbuf = smP ? w.sm->prow : WB(pbuf);
+  uint32_t* rbuf = smP ? w.sm->rbuf : WB(rbuf);
+  uint32_t* qbuf = smQ ? w.sm->qrow : WB(qbuf);
   uint32_t* lbuf = w.sm->lbuf;
   for (uint32_t jb = i + 1; jb < nP; jb += 32) {
     uint32_t j = jb + lane;
@@ -1800,9 +1885,13 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
       kbuf[idx] = order_key(p.order, c, v, k);
       vbuf[idx] = idx;
-      uint32_t out[4];
-      mbe_compress_apply_w<W>(cmp, r.w, out);
-      for (uint32_t q = 0; q < Wn; ++q) pbuf[(size_t)idx * Wn + q] = out[q];
+      if constexpr (LAZY) {
+        pbuf[idx] = r.w[0] & Lx.w[0];
+      } else {
+        uint32_t out[4];
+        mbe_compress_apply_w<W>(cmp, r.w, out);
+        for (uint32_t q = 0; q < Wn; ++q) pbuf[(size_t)idx * Wn + q] = out[q];
+      }
     }
     nPc += __popc(bp);
   }
@@ -1846,9 +1935,13 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     uint32_t bq = __ballot_sync(FULLMASK, keep);
     if (keep) {
       uint32_t idx = nQc + __popc(bq & lanemask_lt());
-      uint32_t out[4];
-      mbe_compress_apply_w<W>(cmp, r.w, out);
-      for (uint32_t q = 0; q < Wn; ++q) qbuf[(size_t)idx * Wn + q] = out[q];
+      if constexpr (LAZY) {
+        qbuf[idx] = r.w[0] & Lx.w[0];
+      } else {
+        uint32_t out[4];
+        mbe_compress_apply_w<W>(cmp, r.w, out);
+        for (uint32_t q = 0; q < Wn; ++q) qbuf[(size_t)idx * Wn + q] = out[q];
+      }
     }
     nQc += __popc(bq);
   }
@@ -1878,6 +1971,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
       }
     }
     if (!dom) {
+      if constexpr (LAZY) r2[0] = mbe_compress_apply(cmp.c[0], r2[0]);  // L'' in L' coordinates
       unsigned long long sL2 = 0;
       uint32_t k2 = 0, before = 0;
       for (uint32_t q = 0; q < Wn; ++q) {
@@ -1885,7 +1979,7 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
         if ((wd >> lane) & 1u) {
           const uint32_t id = lbuf[q * 32 + lane];
           sL2 += g.hvV[id];
-          if (MBE_CAP_RECORDS) w.touched[before + __popc(wd & lanemask_lt())] = id;
+          if (MBE_CAP_RECORDS) WB(touched)[before + __popc(wd & lanemask_lt())] = id;
         }
         before += __popc(wd);
         k2 += __popc(wd);
@@ -1895,24 +1989,35 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
       if (MBE_CAP_RECORDS) {
         if (lane == 0) rbuf[nRx] = x2;
         __syncwarp();
-        write_record(w.lane, p, w.touched, k2, R, nR, x, rbuf, nRx + 1);
+        write_record(w.lane, p, WB(touched), k2, R, nR, x, rbuf, nRx + 1);
       }
     }
+    MBE_PHASE(14, tph);
+    return;
+  }
+  // Eager Step 3 for every child task on the scratch rows (raw Q' candidates decide exactly as
+  // their antichain does), before anything is written: most children end here with no survivor.
+  // The Q' part first, on the unsorted candidates: when it leaves none, no ordering is needed.
+  __syncwarp();
+  const uint32_t nQa = Wn == 1   ? prune_q_mark<1>(pbuf, vbuf, nPc, qbuf, nQc, lane)
+                       : Wn == 2 ? prune_q_mark<2>(pbuf, vbuf, nPc, qbuf, nQc, lane)
+                                 : prune_q_mark<4>(pbuf, vbuf, nPc, qbuf, nQc, lane);
+  if (nQa == 0) {
+    MBE_PHASE(15, tph);
+    account_children(w, p, nPc, 0, Wn, MBE_STATS_ON ? stats_r1_size(Wn, qbuf, nQc, w, p) : 0u);
     MBE_PHASE(14, tph);
     return;
   }
   if (smP) sort_pairs_small(kbuf, vbuf, nPc, w.sm, lane);
   else warp_sort_pairs(w, p, nPc, k);
   MBE_PHASE(13, tph);
-
-  // Eager Step 3 for every child task on the scratch rows (raw Q' candidates decide exactly as
-  // their antichain does), before anything is written: most children end here with no survivor.
-  uint32_t* Stmp = w.touched;
+  // R2 (identical earlier sibling) on the ordered candidates; the Q' decisions ride along in vbuf
+  uint32_t* Stmp = WB(touched);
   __syncwarp();
   const bool asc = p.order == 0u;
-  const uint32_t nS = Wn == 1   ? prune_frame<1>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane, asc)
-                      : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane, asc)
-                                : prune_frame<4>(pbuf, vbuf, nPc, qbuf, nQc, Stmp, lane, asc);
+  const uint32_t nS = Wn == 1   ? prune_frame<1>(pbuf, vbuf, nPc, qbuf, 0u, Stmp, lane, asc)
+                      : Wn == 2 ? prune_frame<2>(pbuf, vbuf, nPc, qbuf, 0u, Stmp, lane, asc)
+                                : prune_frame<4>(pbuf, vbuf, nPc, qbuf, 0u, Stmp, lane, asc);
   MBE_PHASE(15, tph);
   if (nS == 0) {
     account_children(w, p, nPc, 0, Wn, MBE_STATS_ON ? stats_r1_size(Wn, qbuf, nQc, w, p) : 0u);
@@ -1922,17 +2027,21 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
 
   const uint64_t need = MBE_HDR_WORDS + k + nRp + 4 + (uint64_t)nPc * (1 + Wn) + (uint64_t)nQc * Wn + nS;
   if (!arena_reserve(w, p, need)) return;
-  uint32_t* C = w.arena + w.atop;
+  uint32_t* C = WB(arena) + w.atop;
   uint32_t* CL = C + MBE_HDR_WORDS;
   uint32_t* CR = CL + k;
   uint32_t* CP = CR + nRp;
   for (uint32_t t = lane; t < k; t += 32) CL[t] = lbuf[t];
   for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : rbuf[t - nR - 1]);
   for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, kbuf[t]);
-  uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
+  uint32_t* CPr = WB(arena) + align4(w.atop + (CP + nPc - C));
   for (uint32_t t = lane; t < nPc; t += 32) {
-    uint32_t src = vbuf[t];
-    for (uint32_t q = 0; q < Wn; ++q) CPr[(size_t)t * Wn + q] = pbuf[(size_t)src * Wn + q];
+    uint32_t src = vbuf[t] & PERM_IDX;
+    if constexpr (LAZY) {
+      CPr[t] = mbe_compress_apply(cmp.c[0], pbuf[src]);
+    } else {
+      for (uint32_t q = 0; q < Wn; ++q) CPr[(size_t)t * Wn + q] = pbuf[(size_t)src * Wn + q];
+    }
   }
   uint32_t* CQ = CPr + (size_t)nPc * Wn;
   __syncwarp();
@@ -1941,9 +2050,13 @@ __device__ __forceinline__ void bitmap_task(Warp& w, const SearchParams& p, cons
     // reduce into shared memory (skey storage is free again), then copy the survivors out
     uint32_t* kept = reinterpret_cast<uint32_t*>(w.sm->skey);
     nQk = antichain_w(Wn, qbuf, nQc, kept, false, lane, w.sm);
-    for (uint32_t t = lane; t < nQk * Wn; t += 32) CQ[t] = kept[t];
+    for (uint32_t t = lane; t < nQk * Wn; t += 32) CQ[t] = LAZY ? mbe_compress_apply(cmp.c[0], kept[t]) : kept[t];
   } else {
     nQk = antichain_w(Wn, qbuf, nQc, CQ, (p.flags & F_NO_ANTICHAIN) != 0, lane, w.sm);
+    if constexpr (LAZY) {
+      for (uint32_t t = lane; t < nQk; t += 32) CQ[t] = mbe_compress_apply(cmp.c[0], CQ[t]);
+      __syncwarp();
+    }
   }
   account_children(w, p, nPc, nS, Wn, nQk);
   uint32_t* S = CQ + (size_t)nQk * Wn;
@@ -2035,14 +2148,14 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     const bool isPc = valid && c > 0 && c < k;
     if (isExp) sRx += g.hvU[v];
     const uint32_t be = __ballot_sync(FULLMASK, isExp);
-    if (isExp) w.rbuf[nRx + __popc(be & lanemask_lt())] = v;
+    if (isExp) WB(rbuf)[nRx + __popc(be & lanemask_lt())] = v;
     nRx += __popc(be);
     const uint32_t bp = __ballot_sync(FULLMASK, isPc);
     if (isPc) {
       const uint32_t idx = nPc + __popc(bp & lanemask_lt());
-      w.skey[idx] = order_key(p.order, c, v, k);
-      w.sval[idx] = idx;
-      w.pbuf[idx] = j;
+      WB(skey)[idx] = order_key(p.order, c, v, k);
+      WB(sval)[idx] = idx;
+      WB(pbuf)[idx] = j;
     }
     nPc += __popc(bp);
   }
@@ -2057,7 +2170,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
     if (bit) {
       const uint32_t id = L[q * 32 + lane];
       sL += g.hvV[id];
-      w.lbuf[rank] = id;
+      WB(lbuf)[rank] = id;
     }
     before += __popc(word);
   }
@@ -2066,7 +2179,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   const uint32_t nRp = nR + 1 + nRx;
   const uint64_t sRp = sR + g.hvU[x] + sRx;
   account_emit(w, p, sL, k, sRp, nRp);
-  if (MBE_CAP_RECORDS) write_record(w.lane, p, w.lbuf, k, R, nR, x, w.rbuf, nRx);
+  if (MBE_CAP_RECORDS) write_record(w.lane, p, WB(lbuf), k, R, nR, x, WB(rbuf), nRx);
   MBE_PHASE(12, tph);
   if (nPc == 0) return;
 
@@ -2085,7 +2198,7 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
       }
     }
     const uint32_t bq = __ballot_sync(FULLMASK, keep);
-    if (keep) w.qbuf[nQc + __popc(bq & lanemask_lt())] = off;
+    if (keep) WB(qbuf)[nQc + __popc(bq & lanemask_lt())] = off;
     nQc += __popc(bq);
   }
   __syncwarp();
@@ -2104,29 +2217,29 @@ __device__ __forceinline__ void bitmap_task_wide(Warp& w, const SearchParams& p,
   const uint32_t Wn = mbe_words_for(k);
   const uint64_t need = MBE_HDR_WORDS + k + nRp + 8 + (uint64_t)nPc * (2 + Wn) + 2ull * nQc * Wn;
   if (!arena_reserve(w, p, need)) return;
-  uint32_t* C = w.arena + w.atop;
+  uint32_t* C = WB(arena) + w.atop;
   uint32_t* CL = C + MBE_HDR_WORDS;
   uint32_t* CR = CL + k;
   uint32_t* CP = CR + nRp;
-  for (uint32_t t = lane; t < k; t += 32) CL[t] = w.lbuf[t];
-  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : w.rbuf[t - nR - 1]);
-  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, w.skey[t]);
-  uint32_t* CPr = w.arena + align4(w.atop + (CP + nPc - C));
+  for (uint32_t t = lane; t < k; t += 32) CL[t] = WB(lbuf)[t];
+  for (uint32_t t = lane; t < nRp; t += 32) CR[t] = t < nR ? R[t] : (t == nR ? x : WB(rbuf)[t - nR - 1]);
+  for (uint32_t t = lane; t < nPc; t += 32) CP[t] = key_id(p.order, WB(skey)[t]);
+  uint32_t* CPr = WB(arena) + align4(w.atop + (CP + nPc - C));
   uint32_t* cm = reinterpret_cast<uint32_t*>(w.sm->posv);  // compression masks (posv is free here)
   compress_prep_lanes(lx, W, cm, lane);
   const uint32_t prow_off = (uint32_t)(Prow - F);
-  for (uint32_t t = lane; t < nPc; t += 32) w.touched[t] = prow_off + w.pbuf[w.sval[t]] * W;
+  for (uint32_t t = lane; t < nPc; t += 32) WB(touched)[t] = prow_off + WB(pbuf)[WB(sval)[t]] * W;
   __syncwarp();
-  compress_rows_lanes(F, w.touched, nPc, W, lx, cm, Wn, CPr, lane);
+  compress_rows_lanes(F, WB(touched), nPc, W, lx, cm, Wn, CPr, lane);
   uint32_t* CQ = CPr + (size_t)nPc * Wn;
   uint32_t* scratch = CQ + (size_t)nQc * Wn;  // compressed Q' candidates, reduced into CQ below
-  compress_rows_lanes(F, w.qbuf, nQc, W, lx, cm, Wn, scratch, lane);
+  compress_rows_lanes(F, WB(qbuf), nQc, W, lx, cm, Wn, scratch, lane);
   __syncwarp();
   // eager Step 3 against the raw Q' candidates; the antichain only for frames that survive
-  uint32_t* Stmp = w.touched;
+  uint32_t* Stmp = WB(touched);
   MBE_PHASE(14, tph);
   wide_sub(29);
-  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, w.skey, w.pbuf, lane, nullptr, p.order == 0u);
+  const uint32_t nS = prune_frame_w(Wn, CPr, nPc, scratch, nQc, Stmp, WB(skey), WB(pbuf), lane, nullptr, p.order == 0u);
   MBE_PHASE(15, tph);
   wide_sub(30);
   if (nS == 0) {
@@ -2195,11 +2308,27 @@ __device__ __forceinline__ unsigned long long stats_clock(const SearchParams& p)
   return MBE_STATS_ON ? (unsigned long long)clock64() : 0ull;
 }
 
+// The out-of-line routines below take only the fields they use, by value: taking the address of the
+// kernel's SearchParams would force a local-memory copy of it, read back (LDL) on every hot-path use.
+struct StealCtx {
+  uint32_t n_warps;
+  unsigned int* hint;
+  unsigned int* tops;
+  Desc* desc;
+  Globals* gl;
+};
+struct ClaimCtx {
+  Globals* gl;
+  unsigned long long* claim_counter;
+  unsigned long long* claim_tab;
+  uint32_t n_roots, gss_div;
+};
+
 // Idle warp: look for a published frame with unclaimed tasks in the warps
 // advertised by the hint bitmap, scanning circularly from gw+1,
 // and claim ONE task of the bottom-most such frame (largest subtree).
 // Returns true with (*victim, *depth, *task) on success.
-__device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const SearchParams& p, uint32_t rot,
+__device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const StealCtx p, uint32_t rot,
                                        bool steal_half, uint32_t* victim, uint32_t* depth, uint32_t* task,
                                        uint32_t* task_end) {
   const uint32_t nw = (p.n_warps + 31) >> 5;
@@ -2285,9 +2414,9 @@ __device__ __noinline__ bool try_steal(const int lane, const uint32_t gw, const 
 // publication.  The table doubles as the claim log: a relaunch after an arena overflow starts with the
 // previous launch's claim_state, so it replays exactly the chunks this call already took.
 // Lane 0 only.  Returns the global root position, or ~0u when this rank has no more.
-__device__ __noinline__ uint32_t claim_root_shared(const SearchParams& p) {
+__device__ __noinline__ uint32_t claim_root_shared(const ClaimCtx p) {
   const uint32_t i = atomicAdd(&p.gl->lpos, 1u);
-  const uint32_t n = p.g.n_roots;
+  const uint32_t n = p.n_roots;
   for (;;) {
     const unsigned long long s = ld_volatile64(&p.gl->claim_state);
     const uint32_t known = (uint32_t)s;
@@ -2327,18 +2456,15 @@ __device__ __noinline__ uint32_t claim_root_shared(const SearchParams& p) {
 }
 
 // No-progress watchdog (lane 0): true once no warp has completed a task for p.watchdog_ns.
-struct Watch {
-  unsigned long long seen, since;
-};
-__device__ __forceinline__ bool watchdog_expired(const SearchParams& p, Watch& wd) {
+__device__ __forceinline__ bool watchdog_expired(const SearchParams& p, WarpSmem* sm) {
   if (p.watchdog_ns == 0) return false;
   const unsigned long long pr = ld_volatile64(&p.gl->progress), now = globaltimer_ns();
-  if (pr != wd.seen) {
-    wd.seen = pr;
-    wd.since = now;
+  if (pr != sm->wd_seen) {
+    sm->wd_seen = pr;
+    sm->wd_since = now;
     return false;
   }
-  return now - wd.since > p.watchdog_ns;
+  return now - sm->wd_since > p.watchdog_ns;
 }
 
 // ================================================================== kernel
@@ -2353,17 +2479,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
   w.lane = lane;
   w.gw = gw;
   uint8_t* base = p.ws + (size_t)gw * p.ws_stride;
-  w.slot = reinterpret_cast<uint32_t*>(base + p.o_slot);
-  w.sext = reinterpret_cast<uint32_t*>(base + p.o_sext);
-  w.touched = reinterpret_cast<uint32_t*>(base + p.o_touched);
-  w.lbuf = reinterpret_cast<uint32_t*>(base + p.o_lbuf);
-  w.rbuf = reinterpret_cast<uint32_t*>(base + p.o_rbuf);
-  w.skey = reinterpret_cast<unsigned long long*>(base + p.o_skey);
-  w.sval = reinterpret_cast<uint32_t*>(base + p.o_sval);
-  w.pbuf = reinterpret_cast<uint32_t*>(base + p.o_pbuf);
-  w.qbuf = reinterpret_cast<uint32_t*>(base + p.o_qbuf);
-  w.arena = reinterpret_cast<uint32_t*>(base + p.o_arena);
-  w.arena_words = p.arena_words;
+  w.base = base;
   w.desc = p.desc + (size_t)gw * MBE_MAXDEPTH;
   w.top = 0;
   w.atop = 0;
@@ -2380,15 +2496,16 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
   if (lane == 0) {
     for (int k = 0; k < 16; ++k) w.sm->ph[k] = 0;
     w.sm->fc_depth = -1;
+    w.sm->wd_seen = ~0ull;
+    w.sm->wd_since = globaltimer_ns();
   }
   __syncwarp();
 
   const bool steal = !(p.flags & F_NO_STEAL);
   const unsigned long long t_start = globaltimer_ns();
   const unsigned long long c_start = (unsigned long long)clock64();
-  Watch wd{~0ull, t_start};
   uint32_t done_tasks = 0;
-  unsigned long long roots = 0;
+  uint32_t roots = 0;
   bool roots_done = false;
   bool registered = false;
   bool ever_idle = false;
@@ -2437,7 +2554,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         if (lane == 0) {
           dbg_delay(4);
           while (ld_volatile(&dsc->done) < nP - w.sm->ffirst[d]) {
-            if (ld_volatile(&p.gl->error) || watchdog_expired(p, wd)) {
+            if (ld_volatile(&p.gl->error) || watchdog_expired(p, w.sm)) {
               set_error(p, 4u, 1ull);
               w.failed = true;
               break;
@@ -2461,7 +2578,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         nxt = atomicAdd(&dsc->claim, (unsigned long long)k2);
         w.sm->pendk[d] = k2;
       }
-      F = w.arena + w.sm->foff[d];
+      F = WB(arena) + w.sm->foff[d];
       const uint32_t fsz = w.sm->fsz[d];
       if (fsz <= FC_WORDS) {
         if (w.sm->fc_depth != (int)d) {  // (re)load the top frame into shared memory
@@ -2480,7 +2597,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       unsigned long long pos = 0;
       if (lane == 0) {
         if (p.claim_counter) {
-          const uint32_t q = claim_root_shared(p);
+          const uint32_t q = claim_root_shared(ClaimCtx{p.gl, p.claim_counter, p.claim_tab, p.g.n_roots, p.gss_div});
           pos = q == ~0u ? ~0ull : q;
         } else {
           dbg_delay(5);
@@ -2508,7 +2625,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       uint32_t stop = 0;
       if (lane == 0) {
         stop = (ld_volatile(&p.gl->idle) >= p.n_warps) || ld_volatile(&p.gl->error);
-        if (!stop && watchdog_expired(p, wd)) {
+        if (!stop && watchdog_expired(p, w.sm)) {
           set_error(p, 4u, 0ull);  // no-progress watchdog: never hang the device
           stop = 1;
         }
@@ -2518,7 +2635,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
       bool got = false;
       if (steal) {
         // leaves the idle set only on a successful claim
-        got = try_steal(lane, gw, p, rot, (p.flags & F_STEAL_HALF) && !(p.flags & F_STEAL_ONE), &v, &vdep, &ti, &tend);
+        got = try_steal(lane, gw, StealCtx{p.n_warps, p.hint, p.tops, p.desc, p.gl}, rot, (p.flags & F_STEAL_HALF) && !(p.flags & F_STEAL_ONE), &v, &vdep, &ti, &tend);
         rot += 97;
       }
       if (!got) {
@@ -2546,7 +2663,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
         const uint32_t fsz = ld_volatile(&dsc->size);
         if (!arena_reserve(w, p, fsz + 8)) break;
         const uint4* src = reinterpret_cast<const uint4*>(F);
-        uint4* dst = reinterpret_cast<uint4*>(w.arena + w.atop);
+        uint4* dst = reinterpret_cast<uint4*>(WB(arena) + w.atop);
         for (uint32_t t = lane; t < (fsz + 3) / 4; t += 32) dst[t] = src[t];
         __syncwarp();
         if (lane == 0) {
@@ -2608,7 +2725,7 @@ __global__ void __launch_bounds__(MBE_BLOCK, MBE_MINBLOCKS) mbe_search_kernel(Se
     atomicAdd(&p.gl->tasks, WACC(tasks));
     atomicAdd(&p.gl->pruned, WACC(pruned));
     atomicAdd(&p.gl->steals, WACC(steals));
-    if (roots) atomicAdd(&p.gl->roots_run, roots);
+    if (roots) atomicAdd(&p.gl->roots_run, (unsigned long long)roots);
     if MBE_STATS_ON {
       // per-warp workload distribution (Fig. 5 analog): task cycles vs cycles until this warp exits
       const unsigned long long busy = w.sm->ph[0] + w.sm->ph[1] + w.sm->ph[2];
