@@ -11,6 +11,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <chrono>
 #include <cstdio>
@@ -362,16 +363,7 @@ int build_side(mbe_graph* g, int s, uint32_t order = 0) {
   // Σ_{u ∈ N(x)} deg(u), so exact sizes are computed only for candidates, by descending vis, while vis
   // can still beat the best found (a few dozen on power-law graphs).
   {
-    std::vector<std::pair<uint64_t, uint32_t>> heap;
-    heap.reserve(nU);
-    for (uint32_t r = 0; r < nU; ++r) heap.emplace_back(vis[r], r);
-    std::make_heap(heap.begin(), heap.end());
-    std::vector<uint32_t> stamp(nU, 0xffffffffu);
-    uint64_t best = 0;
-    while (!heap.empty() && heap.front().first > best) {
-      const uint32_t r = heap.front().second;
-      std::pop_heap(heap.begin(), heap.end());
-      heap.pop_back();
+    auto two_hop = [&](uint32_t r, std::vector<uint32_t>& stamp) {
       uint64_t two = 0;
       for (uint32_t e = offU[r]; e < offU[r + 1]; ++e)
         for (uint32_t f = offV[adjU[e]]; f < offV[adjU[e] + 1]; ++f)
@@ -379,9 +371,33 @@ int build_side(mbe_graph* g, int s, uint32_t order = 0) {
             stamp[adjV[f]] = r;
             ++two;
           }
-      best = std::max(best, two);
-    }
-    S.cand = best;
+      return two;
+    };
+    uint32_t top = 0;
+    for (uint32_t r = 1; r < nU; ++r)
+      if (vis[r] > vis[top]) top = r;
+    std::vector<uint32_t> stamp0(nU, 0xffffffffu);
+    std::atomic<uint64_t> best(nU ? two_hop(top, stamp0) : 0);
+    std::vector<std::pair<uint64_t, uint32_t>> cand;  // candidates that could still beat it, by descending vis
+    for (uint32_t r = 0; r < nU; ++r)
+      if (r != top && vis[r] > best.load()) cand.emplace_back(vis[r], r);
+    std::sort(cand.begin(), cand.end(), std::greater<>());
+    std::atomic<size_t> next(0);
+    auto worker = [&](std::vector<uint32_t>& stamp) {
+      for (size_t k; (k = next.fetch_add(1)) < cand.size();) {
+        if (cand[k].first <= best.load()) break;  // sorted: no later candidate can beat the best
+        const uint64_t two = two_hop(cand[k].second, stamp);
+        for (uint64_t b = best.load(); two > b && !best.compare_exchange_weak(b, two);) {
+        }
+      }
+    };
+    const unsigned T = std::max(1u, std::min<unsigned>(nth, (unsigned)cand.size()));
+    std::vector<std::thread> th;
+    std::vector<std::vector<uint32_t>> stamps(T > 1 ? T - 1 : 0, std::vector<uint32_t>(nU, 0xffffffffu));
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(worker, std::ref(stamps[t - 1]));
+    worker(stamp0);
+    for (auto& x : th) x.join();
+    S.cand = best.load();
   }
   lap("adjacency");
   // hash terms: side bit 0 for side 1 (rows), 1 for side 2 (cols)
