@@ -270,9 +270,12 @@ def load_ncu(config):
 
     dur = d.get("duration_ms_under_ncu")
     dram = d.get("dram_bytes_per_launch")
+    l2 = d.get("l2_bytes_per_launch")
     lane = num("smsp__thread_inst_executed_per_inst_executed.ratio")
     return {"source": f"profiles/{d.get('name', config)}.md (one serialised launch under ncu)",
             "dram_gbs": dram / dur / 1e6 if dram and dur else None,
+            "l2_gbs": l2 / dur / 1e6 if l2 and dur else None,
+            "icache_hit_pct": num("sm__icc_request_hit_rate.pct"),
             "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "simt_lane_efficiency": lane / 32.0 if lane else None,
             "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),

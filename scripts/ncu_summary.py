@@ -22,6 +22,7 @@ KEYS = [
     "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__icc_request_hit_rate.pct",
 ]
 
 
