@@ -240,7 +240,7 @@ struct Workspace {
   bool busy = false, dirty = true;
   uint32_t n_warps = 0, wmax = 0;
   uint64_t cap_nU = 0, cap_cand = 0, cap_lbuf = 0, arena_bytes = 0, stride = 0;
-  uint64_t o_slot = 0, o_sext = 0, o_touched = 0, o_lbuf = 0, o_rbuf = 0, o_skey = 0, o_sval = 0, o_pbuf = 0, o_qbuf = 0,
+  uint64_t o_slot = 0, o_crow = 0, o_touched = 0, o_lbuf = 0, o_rbuf = 0, o_skey = 0, o_sval = 0, o_pbuf = 0, o_qbuf = 0,
            o_arena = 0;
   DevBuf ws, desc, tops, stamps, hint, per_root, gl;
   void release() {
@@ -458,10 +458,10 @@ uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
 // Per-warp workspace layout (bytes from the warp's base).  The hot, small-index parts of every scratch
 // buffer sit next to each other (arena first, then the candidate-indexed buffers), and the two
-// vertex-indexed tables (slot, sext: random access by vertex id) come last.  `cand` bounds the rows of any
-// one task's candidate buffers (touched, R', sort keys, P'/Q' rows).
+// vertex-indexed slot table (random access by vertex id) comes last.  `cand` bounds the rows of any one
+// task's candidate buffers (the reverse scan's compact bit rows, touched, R', sort keys, P'/Q' rows).
 struct WsLayout {
-  uint64_t slot, sext, touched, lbuf, rbuf, skey, sval, pbuf, qbuf, arena, stride;
+  uint64_t slot, crow, touched, lbuf, rbuf, skey, sval, pbuf, qbuf, arena, stride;
 };
 WsLayout ws_layout(uint64_t nU, uint64_t cand, uint64_t maxdeg, uint64_t arena_bytes, uint32_t wmax) {
   nU = std::max<uint64_t>(nU, 1);
@@ -470,6 +470,7 @@ WsLayout ws_layout(uint64_t nU, uint64_t cand, uint64_t maxdeg, uint64_t arena_b
   WsLayout L;
   uint64_t o = 0;
   L.arena = o; o = align256(o + arena_bytes);
+  L.crow = o; o = align256(o + (wmax > 4 ? cand * 4 * MBE_CROW_WORDS : 0));
   L.touched = o; o = align256(o + cand * 4);
   L.lbuf = o; o = align256(o + lb * 4);
   L.rbuf = o; o = align256(o + cand * 4);
@@ -478,7 +479,6 @@ WsLayout ws_layout(uint64_t nU, uint64_t cand, uint64_t maxdeg, uint64_t arena_b
   L.pbuf = o; o = align256(o + cand * wmax * 4);
   L.qbuf = o; o = align256(o + cand * wmax * 4);
   L.slot = o; o = align256(o + nU * 4 * MBE_SLOT_WORDS);
-  L.sext = o; o = align256(o + nU * 4 * MBE_SEXT_WORDS);
   L.stride = o;
   return L;
 }
@@ -513,7 +513,7 @@ int checkout_workspace(int device, uint32_t n_warps, uint64_t nU, uint64_t cand,
   w->arena_bytes = arena_bytes;
   const WsLayout L = ws_layout(nU, cand, maxdeg, arena_bytes, wmax);
   w->o_slot = L.slot;
-  w->o_sext = L.sext;
+  w->o_crow = L.crow;
   w->o_touched = L.touched;
   w->o_lbuf = L.lbuf;
   w->o_rbuf = L.rbuf;
@@ -923,7 +923,7 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     p.ws = static_cast<uint8_t*>(W->ws.p);
     p.ws_stride = W->stride;
     p.o_slot = W->o_slot;
-    p.o_sext = W->o_sext;
+    p.o_crow = W->o_crow;
     p.o_touched = W->o_touched;
     p.o_lbuf = W->o_lbuf;
     p.o_rbuf = W->o_rbuf;

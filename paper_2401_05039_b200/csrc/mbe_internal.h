@@ -7,8 +7,8 @@
 #define MBE_MAXDEPTH 48    // per-warp stack depth (search depth is 7-11 on C2-C5)
 #endif
 #define MBE_WMAX 16        // bit rows of up to 16 x 32 = 512 columns
-#define MBE_SLOT_WORDS 8   // per-vertex scratch slot: count, -, tag (2), bit row words 0-3 = one 32-B sector
-#define MBE_SEXT_WORDS 12  // per-vertex extension: bit row words 4-15 (wide rows only)
+#define MBE_SLOT_WORDS 8   // per-vertex scratch slot: count, touched index + 1, tag (2), bit-row words 0-3 = one 32-B sector
+#define MBE_CROW_WORDS 12  // per touched vertex (candidate-indexed): bit-row words 4-15 of wide rows
 #ifndef MBE_SMEM_SORT
 #define MBE_SMEM_SORT 128  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
 #endif
@@ -124,7 +124,7 @@ struct SearchParams {
   // per-warp workspace: region w starts at ws + w * ws_stride (bytes); offsets below are bytes
   uint8_t* ws;
   uint64_t ws_stride;
-  uint64_t o_slot, o_sext, o_touched, o_lbuf, o_rbuf, o_skey, o_sval, o_pbuf, o_qbuf, o_arena;
+  uint64_t o_slot, o_crow, o_touched, o_lbuf, o_rbuf, o_skey, o_sval, o_pbuf, o_qbuf, o_arena;
   uint64_t skey2_off;  // element offset of the second (ping-pong) sort buffers
   uint64_t arena_words;
   Desc* desc;          // [n_warps * MBE_MAXDEPTH]

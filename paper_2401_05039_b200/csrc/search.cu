@@ -62,9 +62,6 @@
 #ifndef MBE_COMPRESS_ROWS
 #define MBE_COMPRESS_ROWS 1  // wide column compression: rows per lane in flight (1 with a 2-way word unroll was best; 2 and 4 slower)
 #endif
-#ifndef MBE_EXW_UNROLL
-#define MBE_EXW_UNROLL 0  // 1: copy the staged extension words with compile-time indices
-#endif
 #ifndef MBE_CLS_MLP
 #define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification (2 -> 4: C5 80 -> 68 ms)
 #endif
@@ -156,11 +153,11 @@ struct Warp {
 #endif
 };
 
-// Per-warp buffers (api.cu ws_layout): slot [nU][MBE_SLOT_WORDS] (count, -, tag lo, tag hi, bit row words
-// 0-3: one 32-B sector), sext [nU][MBE_SEXT_WORDS] (bit row words 4-15), touched, lbuf, rbuf, skey, sval,
-// pbuf, qbuf (candidate-indexed) and the frame arena.
+// Per-warp buffers (api.cu ws_layout): slot [nU][MBE_SLOT_WORDS] (count, touched index + 1, tag lo, tag hi,
+// bit-row words 0-3: one 32-B sector per vertex), and candidate-indexed: crow (bit-row words 4-15 of wide
+// rows, in touched order), touched, lbuf, rbuf, skey, sval, pbuf, qbuf, plus the frame arena.
 #define WB_T_slot uint32_t
-#define WB_T_sext uint32_t
+#define WB_T_crow uint32_t
 #define WB_T_touched uint32_t
 #define WB_T_lbuf uint32_t
 #define WB_T_rbuf uint32_t
@@ -1496,22 +1493,41 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
 #pragma unroll
       for (int j = 0; j < MBE_SCAN_MLP; ++j) old[j] = fv[j] ? atomicAdd(&WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS], 1u) : 1u;
       }
+      // discovery: a vertex's first visit gets the next touched index t; words 0-3 of its bit row live in
+      // its slot sector, words 4-15 of a wide row in the candidate-indexed crow[t] (zeroed here; t is
+      // recorded in the slot so later visits find it)
+      uint32_t tj[MBE_SCAN_MLP];
+#pragma unroll
+      for (int j = 0; j < MBE_SCAN_MLP; ++j) {
+        const bool isnew = old[j] == 0u;
+        const uint32_t b = __ballot_sync(FULLMASK, isnew);
+        tj[j] = nt + __popc(b & lanemask_lt());
+        if (isnew) {
+          WB(touched)[tj[j]] = vv[j];
+          if (Wc > 4) {
+            WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS + 1] = tj[j] + 1u;
+            uint4* cr = reinterpret_cast<uint4*>(WB(crow) + (size_t)tj[j] * MBE_CROW_WORDS);
+            for (uint32_t q = 4; q < Wc; q += 4) cr[(q - 4) >> 2] = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+        nt += __popc(b);
+      }
       if (bm && !(MBE_INSTR && (p.flags & F_NO_RS))) {
 #pragma unroll
         for (int j = 0; j < MBE_SCAN_MLP; ++j)
-          if (fv[j]) {
-            const uint32_t q = pos[j] >> 5;
-            uint32_t* wd = q < 4 ? &WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + q]
-                                 : &WB(sext)[(size_t)vv[j] * MBE_SEXT_WORDS + q - 4];
-            atomicOr(wd, 1u << (pos[j] & 31));
-          }
-      }
+          if (fv[j] && pos[j] < 128u)
+            atomicOr(&WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS + 4 + (pos[j] >> 5)], 1u << (pos[j] & 31));
+        if (Wc > 4) {
+          // columns >= 128: the row's index comes from this iteration's discoveries (ordered by the
+          // __syncwarp) or an earlier one, read from L2
+          __syncwarp();
 #pragma unroll
-      for (int j = 0; j < MBE_SCAN_MLP; ++j) {
-        bool isnew = old[j] == 0u;
-        uint32_t b = __ballot_sync(FULLMASK, isnew);
-        if (isnew) WB(touched)[nt + __popc(b & lanemask_lt())] = vv[j];
-        nt += __popc(b);
+          for (int j = 0; j < MBE_SCAN_MLP; ++j)
+            if (fv[j] && pos[j] >= 128u) {
+              const uint32_t t = old[j] != 0u ? __ldcg(&WB(slot)[(size_t)vv[j] * MBE_SLOT_WORDS + 1]) - 1u : tj[j];
+              atomicOr(&WB(crow)[(size_t)t * MBE_CROW_WORDS + (pos[j] >> 5) - 4], 1u << (pos[j] & 31));
+            }
+        }
       }
     }
   }
@@ -1540,7 +1556,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
           ++c;
           if (bm) {
             const uint32_t q = lo >> 5;
-            uint32_t* wd = q < 4 ? &WB(slot)[(size_t)v * MBE_SLOT_WORDS + 4 + q] : &WB(sext)[(size_t)v * MBE_SEXT_WORDS + q - 4];
+            uint32_t* wd = q < 4 ? &WB(slot)[(size_t)v * MBE_SLOT_WORDS + 4 + q] : &WB(crow)[(size_t)t * MBE_CROW_WORDS + q - 4];
             *wd |= 1u << (lo & 31);
           }
         }
@@ -1594,6 +1610,7 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     const uint32_t c = sa[j].x;
     const unsigned long long tg = ((unsigned long long)sa[j].w << 32) | sa[j].z;
     const uint32_t rw[4] = {sb[j].x, sb[j].y, sb[j].z, sb[j].w};
+    const uint32_t* crw = WB(crow) + (size_t)(tb + 32 * j + lane) * MBE_CROW_WORDS - 4;  // words 4.. (touched order)
     // role: 0 none/R, 1 Q-role, 2 P-role
     int role = 0;
     if (valid) {
@@ -1619,36 +1636,16 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
     if (isExp) WB(rbuf)[nRx + __popc(be & lanemask_lt())] = v;
     nRx += __popc(be);
     uint32_t bp = __ballot_sync(FULLMASK, isPc);
-    // words 4.. of a wide (8/16-word) row are still in the slot extension: staged in registers
-    // with vector loads (one round trip), copied to the candidate buffers, then cleared
-    uint32_t* ex = WB(sext) + (size_t)v * MBE_SEXT_WORDS;
-    uint32_t exw[MBE_SEXT_WORDS];
-    if (Wc > 4 && valid) {
-      const uint4* e4 = reinterpret_cast<const uint4*>(ex);
-      const uint4 e0 = e4[0];
-      exw[0] = e0.x; exw[1] = e0.y; exw[2] = e0.z; exw[3] = e0.w;
-      if (Wc > 8) {
-        const uint4 e1 = e4[1], e2 = e4[2];
-        exw[4] = e1.x; exw[5] = e1.y; exw[6] = e1.z; exw[7] = e1.w;
-        exw[8] = e2.x; exw[9] = e2.y; exw[10] = e2.z; exw[11] = e2.w;
-      }
-    }
     if (isPc) {
       uint32_t idx = nPc + __popc(bp & lanemask_lt());
       WB(skey)[idx] = order_key(p.order, c, v, nLp);
       WB(sval)[idx] = idx;
       if (bm) {
-#if MBE_EXW_UNROLL
+        uint32_t* dst = WB(pbuf) + (size_t)idx * Wc;
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q)
-          if (q < Wc) WB(pbuf)[(size_t)idx * Wc + q] = rw[q];
-#pragma unroll
-        for (uint32_t q = 0; q < MBE_SEXT_WORDS; ++q)  // compile-time indices: exw stays in registers
-          if (q + 4 < Wc) WB(pbuf)[(size_t)idx * Wc + q + 4] = exw[q];
-#else
-        for (uint32_t q = 0; q < Wc && q < 4; ++q) WB(pbuf)[(size_t)idx * Wc + q] = rw[q];
-        for (uint32_t q = 4; q < Wc; ++q) WB(pbuf)[(size_t)idx * Wc + q] = exw[q - 4];
-#endif
+          if (q < Wc) dst[q] = rw[q];
+        for (uint32_t q = 4; q < Wc; ++q) dst[q] = crw[q];
       }
     }
     nPc += __popc(bp);
@@ -1656,27 +1653,13 @@ __device__ __forceinline__ void list_task(Warp& w, const SearchParams& p, const 
       uint32_t bq = __ballot_sync(FULLMASK, isQ);
       if (isQ) {
         uint32_t idx = nQc + __popc(bq & lanemask_lt());
-#if MBE_EXW_UNROLL
+        uint32_t* dst = WB(qbuf) + (size_t)idx * Wc;
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q)
-          if (q < Wc) WB(qbuf)[(size_t)idx * Wc + q] = rw[q];
-#pragma unroll
-        for (uint32_t q = 0; q < MBE_SEXT_WORDS; ++q)
-          if (q + 4 < Wc) WB(qbuf)[(size_t)idx * Wc + q + 4] = exw[q];
-#else
-        for (uint32_t q = 0; q < Wc && q < 4; ++q) WB(qbuf)[(size_t)idx * Wc + q] = rw[q];
-        for (uint32_t q = 4; q < Wc; ++q) WB(qbuf)[(size_t)idx * Wc + q] = exw[q - 4];
-#endif
+          if (q < Wc) dst[q] = rw[q];
+        for (uint32_t q = 4; q < Wc; ++q) dst[q] = crw[q];
       }
       nQc += __popc(bq);
-      if (Wc > 4 && valid) {
-        uint4* e4 = reinterpret_cast<uint4*>(ex);
-        e4[0] = make_uint4(0u, 0u, 0u, 0u);
-        if (Wc > 8) {
-          e4[1] = make_uint4(0u, 0u, 0u, 0u);
-          e4[2] = make_uint4(0u, 0u, 0u, 0u);
-        }
-      }
     }
       }
   }

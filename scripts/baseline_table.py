@@ -76,7 +76,7 @@ def main():
               f"{fmt(m.get('lts__t_sector_hit_rate.pct'), '{:.1f} %')} | "
               f"{fmt(m.get('smsp__issue_active.avg.pct_of_peak_sustained_active'), '{:.1f} %')} | "
               f"{fmt((m.get('smsp__thread_inst_executed_per_inst_executed.ratio') or 0) / 32 or None, '{:.2f}')} | "
-              f"{fmt(m.get('sm__icc_request_hit_rate'), '{:.1f} %')} |")
+              f"{fmt(m.get('sm__icc_request_hit_rate.pct'), '{:.1f} %')} |")
 
 
 if __name__ == "__main__":

@@ -309,7 +309,7 @@ def test_shared_counter_overflow_relaunch_replays_claims():
     ctr.close()
 
 
-def _ipc_rank(rank, world, handle_q, out_q):
+def _ipc_rank(rank, world, handle_q, out_q, ack_q):
     import numpy as np  # noqa: F811
 
     from paper_2401_05039_b200 import ClaimCounter, MBEGraph
@@ -321,14 +321,19 @@ def _ipc_rank(rank, world, handle_q, out_q):
         for _ in range(world - 1):
             handle_q.put(ctr.ipc_handle())
     else:
-        ctr = ClaimCounter(0, handle=handle_q.get(timeout=120))
+        ctr = ClaimCounter(0, handle=handle_q.get(timeout=300))
     with MBEGraph.from_graph(g) as G:
         r = G.enumerate(rank=rank, world=world, claim_counter=ctr.ptr)
     out_q.put((rank, r.count, r.hash, r.tasks, r.roots_claimed))
     if rank == 0:
-        out_q.put(("done-wait",))
-        import time
-        time.sleep(3)  # keep the counter alive while the other rank may still use it
+        # keep the counter alive until every other rank is done with it (a spawned rank may take seconds
+        # to import and create its CUDA context, i.e. start after rank 0 has finished)
+        for _ in range(world - 1):
+            ack_q.get(timeout=300)
+    else:
+        ctr.close()
+        ack_q.put(rank)
+        return
     ctr.close()
 
 
@@ -340,15 +345,14 @@ def test_claim_counter_ipc_two_processes_one_gpu():
     g = I.random_bipartite(400, 300, 0.03, 10)
     want = oracle.mbea(g)
     ctx = mp.get_context("spawn")
-    hq, oq = ctx.Queue(), ctx.Queue()
-    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, hq, oq)) for r in range(2)]
+    hq, oq, aq = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, hq, oq, aq)) for r in range(2)]
     [p.start() for p in procs]
     res = {}
     while len(res) < 2:
         item = oq.get(timeout=300)
-        if item[0] != "done-wait":
-            res[item[0]] = item[1:]
-    [p.join(120) for p in procs]
+        res[item[0]] = item[1:]
+    [p.join(300) for p in procs]
     assert all(p.exitcode == 0 for p in procs)
     assert res[0][0] + res[1][0] == want.count
     assert (res[0][1] + res[1][1]) & R.MASK64 == want.hash
@@ -429,3 +433,52 @@ def test_no_reverse_scan_ablation_same_tree():
         assert same(gpu(g, flags=MBE_NO_RS), want), g.name
     g = I.erdos_renyi_c1b(120, 90)
     assert same(gpu(g, flags=MBE_NO_RS, bitmap_threshold=32), oracle.mbea(g))
+
+
+def _two_hop_max(g):
+    """max over candidates x of |N(N(x))| (x included), candidate side = the smaller side (reading Z4)."""
+    rp = np.asarray(g.row_ptr, dtype=np.int64)
+    ci = np.asarray(g.col_idx, dtype=np.int64)
+    rows = np.repeat(np.arange(g.n1), np.diff(rp))
+    cu, cv, nu = (ci, rows, g.n2) if g.n2 < g.n1 else (rows, ci, g.n1)
+    nbr_u = [set() for _ in range(nu)]
+    by_v = {}
+    for u, v in zip(cu.tolist(), cv.tolist()):
+        nbr_u[u].add(v)
+        by_v.setdefault(v, set()).add(u)
+    best, maxdeg = 0, 0
+    for u in range(nu):
+        two = set()
+        for v in nbr_u[u]:
+            two |= by_v[v]
+        best = max(best, len(two))
+        maxdeg = max(maxdeg, len(nbr_u[u]))
+    return best, nu, maxdeg
+
+
+@pytest.mark.parametrize("g", [I.erdos_renyi_c1b(), I.random_bipartite(300, 120, 0.03, 11),
+                               I.random_bipartite(40, 700, 0.3, 4)])
+def test_workspace_sized_by_two_hop_bound(g):
+    """The per-warp candidate buffers hold max_x |N(N(x))| rows: workspace_bytes equals
+    n_warps x the layout stride computed here from an independent 2-hop count (sets, no CSR tricks)."""
+    from paper_2401_05039_b200 import mbe_release_workspaces
+
+    mbe_release_workspaces()  # no pooled (larger) workspace may be reused
+    cand, nu, maxdeg = _two_hop_max(g)
+    with MBEGraph.from_graph(g) as G:
+        want = oracle.mbea(g)
+        r = G.enumerate()
+    assert same(r, want)
+
+    def a256(x):
+        return (x + 255) & ~255
+
+    ne = len(g.col_idx)
+    arena = a256(min(2 << 20, max(256 << 10, 16 * (g.n1 + g.n2 + ne))))
+    wmax = 16  # auto bit-row threshold 512 on an idle B200
+    lb = max(maxdeg, 512)
+    o = a256(arena)
+    for b in (cand * 48, cand * 4, lb * 4, cand * 4, cand * 32, cand * 8, cand * wmax * 4, cand * wmax * 4,
+              nu * 32):
+        o = a256(o + b)
+    assert r.workspace_bytes == o * r.n_warps, (r.workspace_bytes, o * r.n_warps, cand)
