@@ -127,7 +127,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle (cpu_baseline / reference arm)
-def oracle_rate(g, target_s: float, seed: int = 7, config: str = ""):
+def oracle_rate(g, target_s: float, seed: int = 7, config: str = "", parts: int = 1, part_stats=None):
     """Oracle bicliques/s on a bounded, UNBIASED sample of the level-1 subtrees.
 
     The sample is a seeded uniform random 1/k of ALL level-1 subtrees (no exclusion): its expected
@@ -144,26 +144,37 @@ def oracle_rate(g, target_s: float, seed: int = 7, config: str = ""):
     deg = np.bincount(g.col_idx, minlength=g.n2) if side == 2 else np.diff(g.row_ptr.astype(np.int64))
     roots = np.nonzero(deg > 0)[0].astype(np.uint32)
     rng = np.random.default_rng(seed)
+    part_stats = [] if part_stats is None else part_stats
 
-    def run(k):
+    def run_roots(sel):
         import resource
 
-        m = max(1, len(roots) // k)
-        pick = np.sort(rng.choice(len(roots), size=m, replace=False))
         ru0 = resource.getrusage(resource.RUSAGE_SELF)
         t0 = time.perf_counter()
-        pr = oracle.mbea_roots(g, roots[pick], candidate_side=side)
+        pr = oracle.mbea_roots(g, np.sort(sel), candidate_side=side)
         wall = time.perf_counter() - t0
         ru1 = resource.getrusage(resource.RUSAGE_SELF)
         cpu_s = (ru1.ru_utime - ru0.ru_utime) + (ru1.ru_stime - ru0.ru_stime)
-        return int(pr[:, 0].sum()), wall, m, cpu_s
+        return int(pr[:, 0].sum()), wall, cpu_s
+
+    def run(k):
+        m = max(1, len(roots) // k)
+        pick = rng.choice(len(roots), size=m, replace=False)
+        if parts > 1:  # disjoint random parts of the one sample, each run and timed on its own
+            out = [run_roots(roots[pick[j::parts]]) for j in range(parts) if len(pick[j::parts])]
+            part_stats.extend(out)
+            return sum(o[0] for o in out), sum(o[1] for o in out), m, sum(o[2] for o in out)
+        c, wall, cpu_s = run_roots(roots[pick])
+        return c, wall, m, cpu_s
 
     full = golden_full_run(config)
     if full:
         k = max(1, int(round(full["seconds"] * full["threads"] / threads / target_s)))
     else:
         k = max(1, len(roots) // 64)
+        save, parts = parts, 1
         _, _, _, c0 = run(k)
+        parts = save
         k = max(1, int(round(k * c0 / threads / target_s)))
     cnt, dt, m, cpu_s = run(k)
     # rate = count / (thread-seconds / threads): the sample's work spread evenly over the host's cores, as the
@@ -198,16 +209,23 @@ def run_reference(args):
 
     oracle.build_oracle()
     g = graph_of(args.config)
-    per_step_target = max(2.0, min(15.0, 60.0 / max(1, args.steps + args.warmup)))
-    rates, infos = [], []
-    for s in range(args.warmup + args.steps):
-        r, info = oracle_rate(g, per_step_target, seed=7 + s, config=args.config)
-        if s >= args.warmup:
-            rates.append(r)
-            infos.append(info)
-    value = float(np.mean(rates))
-    info = infos[-1]
-    sample = info["sample"] + " per step"
+    # Per-root oracle cost is heavy-tailed (the heaviest C5 subtrees take ~1 min on one thread), so
+    # independent per-step samples would each risk one of them and the K + W run could take tens of
+    # minutes.  Instead ONE seeded uniform random 1/k sample (--ref-seconds, default ~4 s of expected
+    # work on the host's cores) is split into K disjoint random parts, one per timed step (each part is
+    # itself a uniform random sample), so the whole run costs about one such sample; the W warm-up steps
+    # run small samples of their own.  value = the pooled rate of the K parts.
+    for s in range(args.warmup):
+        oracle_rate(g, 0.2, seed=1000 + s, config=args.config)
+    parts = []
+    _, info = oracle_rate(g, args.ref_seconds, seed=7, config=args.config, parts=max(1, args.steps),
+                          part_stats=parts)
+    cnt = sum(p[0] for p in parts)
+    eff = max(sum(p[2] for p in parts) / info["threads"], 1e-9)
+    value = cnt / eff
+    sample = info["sample"].replace("rate = count", f"split into {len(parts)} disjoint random parts, one per timed "
+                                                   f"step; rate = pooled count")
+    infos = [{"seconds": p[1]} for p in parts]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([i["seconds"] for i in infos])),
@@ -484,6 +502,8 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--T", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0,
+                    help="--impl reference: expected oracle work of the one sample split over the K steps (s)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--static-deal", action="store_true", help="multi-rank: deal level-1 subtrees k = rank mod N")
     args = ap.parse_args()

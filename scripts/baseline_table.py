@@ -41,7 +41,7 @@ def ncu_metrics(path):
         except (ValueError, AttributeError):
             continue
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-6,
-                 "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(unit, 1.0)
+                 "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(unit, 1.0)
         out[name] = v * scale
     return out
 
