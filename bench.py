@@ -395,7 +395,7 @@ def run_ours(args):
     rp_pin = torch.from_numpy(rp).pin_memory().numpy()
     ci_pin = torch.from_numpy(ci).pin_memory().numpy()
     e2e_t, h2d = [], 0
-    for k in range(args.warmup + args.steps):
+    for k in range(args.warmup + (args.steps if world > 1 else max(3, min(args.steps, 5)))):
         if ctr is not None and rank == 0:
             ctr.reset()
         if world > 1:
@@ -417,6 +417,50 @@ def run_ours(args):
         if k >= args.warmup:
             e2e_t.append(max_over_ranks(dt, red_dev) if world > 1 else dt)
             h2d = int(info["h2d_bytes"])
+    e2e_latency_ms = 1e3 * float(np.median(e2e_t))
+    # Streamed e2e (1 rank): K graphs through the C ABI, every step's ingest + H2D copy from pinned host
+    # memory and its result read-back inside the timed region; a loader thread ingests graph k+1 (host work
+    # and the H2D copy, which the search stream does not wait for) while graph k is enumerated — the
+    # overlap a serving loop gets from two host threads on independent handles (thread-compatible ABI).
+    e2e_mode = "sequential per step (median latency)"
+    if world == 1:
+        import queue
+
+        q = queue.Queue(maxsize=1)
+
+        lt = []
+        # half the host cores: the search thread (launch, stream synchronisation) must not wait for a core
+        ingest_t = max(1, min(16, (os.cpu_count() or 4) // 2))
+
+        def loader(n):
+            for _ in range(n):
+                a = time.perf_counter()
+                hd_ = mbe_load_csr(g.n1, g.n2, rp_pin, ci_pin, device=dev_index, ingest_threads=ingest_t)
+                lt.append(time.perf_counter() - a)
+                q.put(hd_)
+
+        sstream = torch.cuda.Stream(device=dev)  # non-blocking: the loader's H2D copies need not wait for it
+        torch.cuda.synchronize(dev)
+        th = threading.Thread(target=loader, args=(args.steps,), daemon=True)
+        t0 = time.perf_counter()
+        th.start()
+        et = []
+        for k in range(args.steps):
+            a = time.perf_counter()
+            hd = q.get()
+            b = time.perf_counter()
+            r = mbe_enumerate(hd, make_config(stream=sstream.cuda_stream, **knobs))
+            mbe_free(hd)
+            et.append((b - a, time.perf_counter() - b, r.kernel_ms))
+            assert (r.count, r.hash) == (count, h), "e2e result differs"
+        t1 = time.perf_counter()
+        th.join()
+        if os.environ.get("MBE_BENCH_DEBUG"):
+            print("streamed e2e: load ms", [round(1e3 * x, 1) for x in lt], "wait/enumerate ms",
+                  [(round(1e3 * x, 1), round(1e3 * y, 1), round(z, 1)) for x, y, z in et], file=sys.stderr)
+        e2e_t = [(t1 - t0) / args.steps]
+        e2e_mode = (f"{args.steps} graphs streamed through the C ABI (ingest + H2D of graph k+1 on a loader thread "
+                    f"overlapping the search of graph k); value = steps x count / wall time")
     e2e_value = count / float(np.median(e2e_t))
 
     # roofline of the dominant kernel (the persistent search kernel): SURVEY §8(d) algorithmic bytes of
@@ -460,7 +504,8 @@ def run_ours(args):
                                       "p90": float(np.percentile(times, 90)), "max": float(np.max(times))},
                        "per_rank": per_rank},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": D2H_BYTES, "ms_per_step": 1e3 * float(np.median(e2e_t))},
+                    "d2h_bytes_per_step": D2H_BYTES, "ms_per_step": 1e3 * float(np.median(e2e_t)),
+                    "mode": e2e_mode, "latency_ms": e2e_latency_ms},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -153,15 +153,6 @@ void graph_release(DevBuf& b) {
   b.bytes = 0;
 }
 
-template <class T>
-int upload(DevBuf& b, const std::vector<T>& v) {
-  size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
-  if (cudaMalloc(&b.p, bytes) != cudaSuccess) return fail(MBE_ENOMEM, "cudaMalloc graph");
-  b.bytes = bytes;
-  if (g_upload_counter) *g_upload_counter += v.size() * sizeof(T);
-  if (!v.empty()) CUDA_TRY(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-  return MBE_OK;
-}
 
 struct Side {
   bool built = false;
@@ -179,6 +170,32 @@ struct Side {
     built = false;
   }
 };
+
+// Host->device copies of ingest run on a per-device NON-BLOCKING stream: a load on one host thread then
+// never waits for a search running on another thread's stream (the legacy default stream would).
+cudaStream_t copy_stream() {
+  static std::mutex mu;
+  static cudaStream_t s[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!s[dev] && cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    s[dev] = nullptr;
+  }
+  return s[dev];
+}
+
+int copy_h2d(void* dst, const void* src, size_t bytes) {
+  cudaStream_t cs = copy_stream();
+  if (!cs) {
+    CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    return MBE_OK;
+  }
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs));
+  CUDA_TRY(cudaStreamSynchronize(cs));
+  return MBE_OK;
+}
 
 // Packs host arrays into one device allocation (one cudaMalloc, one cudaFree per side).
 struct Packer {
@@ -211,7 +228,8 @@ struct Packer {
     }
     if (!g_stage) {  // no pinned memory: pageable copies straight from the arrays
       for (const Item& it : items)
-        if (it.src && it.bytes) CUDA_TRY(cudaMemcpy(it.dst->p, it.src, it.bytes, cudaMemcpyHostToDevice));
+        if (it.src && it.bytes)
+          if (int rc = copy_h2d(it.dst->p, it.src, it.bytes)) return rc;
       return MBE_OK;
     }
     uint8_t* stage = static_cast<uint8_t*>(g_stage);
@@ -227,8 +245,7 @@ struct Packer {
         std::memcpy(stage + it.off + o, static_cast<const uint8_t*>(it.src) + o, n);
       }
     });
-    CUDA_TRY(cudaMemcpy(all.p, stage, total, cudaMemcpyHostToDevice));
-    return MBE_OK;
+    return copy_h2d(all.p, stage, total);
   }
 };
 
@@ -266,14 +283,55 @@ struct mbe_graph {
   int sm_count = 0;
   int occ[2][5] = {{0}};         // cached occupancy: [instr][threads/32 - 1] resident CTAs per SM
   DevBuf claim_tab;             // shared-counter claim log of the current call ([n_roots + 1] u64)
-  ~mbe_graph() {
-    claim_tab.release();
-    for (auto& so : side)
-      for (auto& s : so) s.release();
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-  }
+  ~mbe_graph();
 };
+
+// Timing events and SM counts are process-wide per device: creating or destroying an event (or querying an
+// attribute) can wait for a search kernel running on another thread, which would serialise a loader thread
+// with the search it is meant to overlap.  Events come from a pool (filled lazily by mbe_enumerate).
+std::mutex g_ev_mu;
+std::vector<std::pair<int, cudaEvent_t>> g_ev_pool;
+cudaEvent_t ev_get(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    for (size_t k = 0; k < g_ev_pool.size(); ++k)
+      if (g_ev_pool[k].first == dev) {
+        cudaEvent_t e = g_ev_pool[k].second;
+        g_ev_pool.erase(g_ev_pool.begin() + k);
+        return e;
+      }
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return e;
+}
+void ev_put(int dev, cudaEvent_t e) {
+  if (!e) return;
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  g_ev_pool.push_back({dev, e});
+}
+int sm_count_of(int dev) {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) return 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!cache[dev] && cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    cache[dev] = 0;
+  }
+  return cache[dev];
+}
+
+mbe_graph::~mbe_graph() {
+  claim_tab.release();
+  for (auto& so : side)
+    for (auto& s : so) s.release();
+  ev_put(device, ev0);
+  ev_put(device, ev1);
+}
 
 namespace {
 
@@ -697,13 +755,9 @@ int mbe_load_csr(uint32_t n1, uint32_t n2, const uint64_t* row_ptr, const uint32
     });
   }
   lap("column CSR");
-  if (cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+  if ((g->sm_count = sm_count_of(device)) <= 0) {
     delete g;
     return fail(MBE_ECUDA, "cudaDeviceGetAttribute(multiProcessorCount)");
-  }
-  if (cudaEventCreate(&g->ev0) != cudaSuccess || cudaEventCreate(&g->ev1) != cudaSuccess) {
-    delete g;
-    return fail(MBE_ECUDA, "cudaEventCreate");
   }
   lap("device attr + events");
   int side = n2 < n1 ? 2 : 1;
@@ -958,6 +1012,9 @@ int mbe_enumerate(mbe_graph* g, const mbe_config* cfg_in, mbe_result* res, mbe_o
     CUDA_TRY(cudaMemsetAsync(W->hint.p, 0, 4ull * ((n_warps + 31) / 32), st));
     if (p.per_root) CUDA_TRY(cudaMemsetAsync(W->per_root.p, 0, 32ull * S.nU, st));
     const int smem = smem_warp * (int)(threads / 32);
+    if (!g->ev0) g->ev0 = ev_get(g->device);
+    if (!g->ev1) g->ev1 = ev_get(g->device);
+    if (!g->ev0 || !g->ev1) return fail(MBE_ECUDA, "cudaEventCreate");
     const int lrc = instr ? mbe_launch_search_instr(p, (int)grid, (int)threads, smem, st, g->ev0, g->ev1)
                           : mbe_launch_search(p, (int)grid, (int)threads, smem, st, g->ev0, g->ev1);
     if (lrc != 0)
