@@ -15,7 +15,10 @@
  *    exceptions cross the ABI.  On error, *out / *res contents are unspecified
  *    and no handle leaks; mbe_last_error_detail() gives a message.
  *  - Handles are thread-compatible, not re-entrant: do not call two functions
- *    on the same handle concurrently.
+ *    on the same handle concurrently.  Different handles may be used from
+ *    different host threads; mbe_load_csr's host->device copies run on an
+ *    internal non-blocking stream, so loading the next graph on one thread
+ *    overlaps a search running on another (bench.py's streamed e2e).
  *  - No CPU fallback: when no CUDA device is usable, mbe_load_csr returns
  *    MBE_ECUDA.
  */
