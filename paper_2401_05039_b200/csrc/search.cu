@@ -51,7 +51,7 @@
 #define MBE_NARROW_TEMPLATES 0  // bit mask: 2 / 4 = separate register-resident 2- / 4-word task bodies (0: only 1-word; smaller code, C5 -2 %)
 #endif
 #ifndef MBE_SCAN_MLP
-#define MBE_SCAN_MLP 4  // reverse-scan visits in flight per lane
+#define MBE_SCAN_MLP 2  // reverse-scan visits in flight per lane (2 beat 1, 3, 4, 8 at the final build: C5 -3 %, C4 -6 %)
 #endif
 #ifndef MBE_BACKOFF_MIN
 #define MBE_BACKOFF_MIN 64  // ns: first idle back-off after a failed steal attempt
@@ -62,6 +62,10 @@
 #ifndef MBE_COMPRESS_ROWS
 #define MBE_COMPRESS_ROWS 1  // wide column compression: rows per lane in flight (1 with a 2-way word unroll was best; 2 and 4 slower)
 #endif
+#ifndef MBE_COMPRESS_UNROLL
+#define MBE_COMPRESS_UNROLL 2  // word-loop unroll of the wide column compression
+#endif
+constexpr int kCompressUnroll = MBE_COMPRESS_UNROLL;
 #ifndef MBE_CLS_MLP
 #define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification (2 -> 4: C5 80 -> 68 ms)
 #endif
@@ -1082,7 +1086,7 @@ __device__ __noinline__ void compress_rows_lanes(const uint32_t* F, const uint32
       acc[k] = 0u;
       accw[k] = 0u;
     }
-#pragma unroll 2
+#pragma unroll kCompressUnroll
     for (uint32_t q = 0; q < W; ++q) {
       const uint32_t m = lx[q];
       if (m == 0u) continue;  // a zero word of row(x) contributes no column (and no load)
@@ -1150,15 +1154,18 @@ __device__ __forceinline__ void compress_prep_lanes(const uint32_t* lx, uint32_t
 //   (b) some Q row contains r_t.
 // ~93% of all tasks end here, so they are never claimed, cached or dispatched.
 // Writes the surviving task indices (ascending) to S; returns their number.
+#ifndef MBE_QROWS
+#define MBE_QROWS 8  // Q rows loaded per step of the eager check (independent loads in flight)
+#endif
 template <int W>
 __device__ __forceinline__ bool prune_q_rows(const Row<W>& r, bool alive, const uint32_t* Qr, uint32_t nQ) {
-  for (uint32_t qb = 0; qb < nQ; qb += 8) {
+  for (uint32_t qb = 0; qb < nQ; qb += MBE_QROWS) {
     if (!__any_sync(FULLMASK, alive)) break;
-    Row<W> s[8];
+    Row<W> s[MBE_QROWS];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s[u] = qb + u < nQ ? load_row<W>(Qr + (size_t)(qb + u) * W) : zero_row<W>();
+    for (int u = 0; u < MBE_QROWS; ++u) s[u] = qb + u < nQ ? load_row<W>(Qr + (size_t)(qb + u) * W) : zero_row<W>();
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < MBE_QROWS; ++u)
       if (qb + u < nQ && row_subset<W>(r, s[u])) alive = false;
   }
   return alive;
