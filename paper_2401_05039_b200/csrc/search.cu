@@ -63,7 +63,7 @@
 #define MBE_COMPRESS_ROWS 1  // wide column compression: rows per lane in flight (1 with a 2-way word unroll was best; 2 and 4 slower)
 #endif
 #ifndef MBE_COMPRESS_UNROLL
-#define MBE_COMPRESS_UNROLL 2  // word-loop unroll of the wide column compression
+#define MBE_COMPRESS_UNROLL 1  // word-loop unroll of the wide column compression (1 beat 2 and 4: C5 -3 %, C4 -4 %)
 #endif
 constexpr int kCompressUnroll = MBE_COMPRESS_UNROLL;
 #ifndef MBE_CLS_MLP
@@ -1155,7 +1155,7 @@ __device__ __forceinline__ void compress_prep_lanes(const uint32_t* lx, uint32_t
 // ~93% of all tasks end here, so they are never claimed, cached or dispatched.
 // Writes the surviving task indices (ascending) to S; returns their number.
 #ifndef MBE_QROWS
-#define MBE_QROWS 8  // Q rows loaded per step of the eager check (independent loads in flight)
+#define MBE_QROWS 4  // Q rows loaded per step of the eager check (4 beat 6, 8, 16 with the smaller loops: C5 -3 %)
 #endif
 template <int W>
 __device__ __forceinline__ bool prune_q_rows(const Row<W>& r, bool alive, const uint32_t* Qr, uint32_t nQ) {
@@ -1229,6 +1229,9 @@ __device__ __noinline__ uint32_t prune_q_mark(const uint32_t* Pr, uint32_t* val,
 // Wide rows (8/16 words): the same test word-sliced, rows read from memory (L1).  Every row's
 // (popcount, OR-fold) metadata is computed once into `meta` (global scratch, >= nP + nQ entries);
 // its necessary conditions for == and ⊆ filter the pairs, 8 Q rows in flight per step.
+#ifndef MBE_WQROWS
+#define MBE_WQROWS 8  // wide eager check: Q-row metadata words loaded per step
+#endif
 #ifndef MBE_CMASK_MIN
 #define MBE_CMASK_MIN 0xffffffffu  // Q rows above which the wide check transposes Q into column masks (with >= 96 P rows)
 #endif
@@ -1313,13 +1316,13 @@ __device__ __noinline__ uint32_t prune_frame_wide(const uint32_t* Pr, uint32_t n
         if (hit && lane == sl) alive = false;
       }
     }
-    for (uint32_t qb = 0; !cmask && qb < nQ; qb += 8) {
+    for (uint32_t qb = 0; !cmask && qb < nQ; qb += MBE_WQROWS) {
       if (!__any_sync(FULLMASK, alive)) break;
-      unsigned long long m8[8];
+      unsigned long long m8[MBE_WQROWS];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) m8[u] = qb + u < nQ ? mq[qb + u] : ~0ull;
+      for (int u = 0; u < MBE_WQROWS; ++u) m8[u] = qb + u < nQ ? mq[qb + u] : ~0ull;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < MBE_WQROWS; ++u)
         if (alive && qb + u < nQ && meta_may_subset(mr, m8[u]) && wide_subset(r, Qr + (size_t)(qb + u) * W, W))
           alive = false;
     }
