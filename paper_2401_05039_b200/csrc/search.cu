@@ -759,6 +759,9 @@ __device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, ui
 
 // Necessary-condition filters for wide rows: a ⊆ b requires popc(a) <= popc(b) and
 // fold(a) ⊆ fold(b); a == b requires equal metadata.
+#ifndef MBE_META_ROLL
+#define MBE_META_ROLL 0  // 1: the wide-row metadata loop is not unrolled
+#endif
 #if MBE_META54
 // fold = OR of the row's 64-bit halves (54 buckets kept); meta = (popc << 54) | fold
 #define MBE_META_SHIFT 54
@@ -766,9 +769,14 @@ __device__ __forceinline__ bool wide_eq(const uint32_t* a, const uint32_t* b, ui
 __device__ __forceinline__ unsigned long long wide_meta(const uint32_t* r, uint32_t W) {
   uint32_t pc = 0;
   unsigned long long f = 0;
+#if MBE_META_ROLL
+#pragma unroll 1
+  for (uint32_t q = 0; q < W; q += 4) {
+#else
 #pragma unroll
   for (uint32_t q = 0; q < MBE_WMAX; q += 4)
     if (q < W) {
+#endif
       const uint4 u = *reinterpret_cast<const uint4*>(r + q);
       pc += __popc(u.x) + __popc(u.y) + __popc(u.z) + __popc(u.w);
       f |= ((unsigned long long)u.y << 32 | u.x) | ((unsigned long long)u.w << 32 | u.z);
