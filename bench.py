@@ -435,7 +435,11 @@ def run_ours(args):
         def loader(n):
             for _ in range(n):
                 a = time.perf_counter()
-                hd_ = mbe_load_csr(g.n1, g.n2, rp_pin, ci_pin, device=dev_index, ingest_threads=ingest_t)
+                try:
+                    hd_ = mbe_load_csr(g.n1, g.n2, rp_pin, ci_pin, device=dev_index, ingest_threads=ingest_t)
+                except BaseException as exc:  # handed to the search thread, which re-raises it
+                    q.put(exc)
+                    return
                 lt.append(time.perf_counter() - a)
                 q.put(hd_)
 
@@ -447,7 +451,9 @@ def run_ours(args):
         et = []
         for k in range(args.steps):
             a = time.perf_counter()
-            hd = q.get()
+            hd = q.get(timeout=600)
+            if isinstance(hd, BaseException):
+                raise hd
             b = time.perf_counter()
             r = mbe_enumerate(hd, make_config(stream=sstream.cuda_stream, **knobs))
             mbe_free(hd)
