@@ -13,14 +13,15 @@
 #define MBE_SMEM_SORT 128  // pairs sorted in shared memory per warp; larger sorts use radix in HBM
 #endif
 #define MBE_HDR_WORDS 8    // frame header
-// Persistent launch shape: 128-thread CTAs, 7 per SM (72 registers/thread, 28 warps/SM, 6.6 KB of
-// shared memory per warp): on C4/C5 7 CTAs beat 6 (85 registers) by 4-5 % and 8 (64 registers,
-// spills) lost 30 % on C4 (profiles/ab_r2_occupancy.jsonl).
+// Persistent launch shape: 128-thread CTAs, 6 per SM (85 registers/thread, 24 warps/SM).  Early in round 2
+// 7 CTAs (72 registers) were 4-5 % faster; once the hot loops were made smaller (scan MLP 2, rolled wide
+// compression, 4 Q rows per eager-check step) 6 CTAs measured 1-4 % faster on C3/C5/C5p and equal on C4,
+// with 1/7 less workspace (profiles/ab_r2_session2.jsonl); 8 (64 registers) stays slower.
 #ifndef MBE_BLOCK
 #define MBE_BLOCK 128
 #endif
 #ifndef MBE_MINBLOCKS
-#define MBE_MINBLOCKS 7
+#define MBE_MINBLOCKS 6
 #endif
 
 // Relocalization / reduction thresholds (build-time tuning constants; result-invariant).
