@@ -482,3 +482,39 @@ def test_workspace_sized_by_two_hop_bound(g):
               nu * 32):
         o = a256(o + b)
     assert r.workspace_bytes == o * r.n_warps, (r.workspace_bytes, o * r.n_warps, cand)
+
+
+def test_concurrent_load_and_enumerate_on_two_threads():
+    """The streamed e2e pattern (bench.py): one host thread loads the next graph (ingest + H2D on the library's
+    non-blocking copy stream) while another enumerates the current one; every result stays exact."""
+    import threading
+
+    import torch
+
+    from paper_2401_05039_b200 import make_config, mbe_enumerate, mbe_free, mbe_load_csr
+
+    graphs = [I.random_bipartite(300, 200, 0.04, 31 + k) for k in range(6)]
+    want = [oracle.mbea(g) for g in graphs]
+    stream = torch.cuda.Stream()
+    handles, errors = [None] * len(graphs), []
+
+    def loader():
+        try:
+            for k, g in enumerate(graphs):
+                handles[k] = mbe_load_csr(g.n1, g.n2, g.row_ptr, g.col_idx, device=0, ingest_threads=2)
+                ready[k].set()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+            for ev in ready:
+                ev.set()
+
+    ready = [threading.Event() for _ in graphs]
+    th = threading.Thread(target=loader)
+    th.start()
+    for k in range(len(graphs)):
+        assert ready[k].wait(120)
+        assert not errors, errors
+        r = mbe_enumerate(handles[k], make_config(stream=stream.cuda_stream))
+        mbe_free(handles[k])
+        assert (r.count, r.hash, r.tasks, r.pruned) == (want[k].count, want[k].hash, want[k].tasks, want[k].pruned)
+    th.join()
