@@ -67,7 +67,7 @@
 #endif
 constexpr int kCompressUnroll = MBE_COMPRESS_UNROLL;
 #ifndef MBE_CLS_MLP
-#define MBE_CLS_MLP 4   // touched-vertex slots in flight per lane during classification (2 -> 4: C5 80 -> 68 ms)
+#define MBE_CLS_MLP 5  // touched-vertex slots in flight per lane during classification (r1: 2 -> 4, C5 80 -> 68 ms; r2 at 6 CTAs/SM: 5 beat 4 and 6, C4 -4.5 %, C3 -5 %, C5 -1.4 %)
 #endif
 #ifndef MBE_DEBUG_DELAYS
 #define MBE_DEBUG_DELAYS 0  // 1: random __nanosleep at the claim / steal / publish / pop points (race stress builds)
